@@ -1,0 +1,451 @@
+"""bench.py -- fused RGB-D GMM segmentation throughput on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload streams256|vga|hd1080|rows8k] [--variant auto|ldg|ldg_elide]
+
+One step = one frame of every camera stream of the workload pushed through
+the hot path (colour GMM + depth GMM + List-1 fusion, processor.cpp:158-184).
+Default workload = BASELINE.json configs[3]: 256 concurrent 640x480 RGB-D
+streams, M=5, batched, sharded by stream across the N GPUs of the box (total
+work fixed -> "scaling": "strong").  Synthetic scenario-A frames (seeds 1..256)
+are rendered on the GPU before timing.  Prints ONE JSON line on rank 0.
+
+`value` = whole-job Mpix/s with frames resident in HBM (CUDA events on the
+kernel stream, max over ranks); `e2e` = the same metric through the public
+API from pinned host frames with the fused masks read back every step;
+`roofline` = the fused kernel's algorithmic bytes / its event-timed duration
+against MEASURED_PEAKS.json; `cpu_baseline` = the reference compiled from
+source (oracle/_ref) on this host's cores on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (config text, width, height, streams, M, shard)
+    "streams256": ("256 concurrent 640x480 RGB-D streams batched, sharded by stream",
+                   640, 480, 256, 5, "stream"),
+    "vga": ("640x480 RGB+depth, M=5, separate GMMs + fusion, single stream per GPU",
+            640, 480, 1, 5, "replica"),
+    "hd1080": ("1920x1080 RGB-D, M=5, illumination change + shadows, one stream per GPU",
+               1920, 1080, 1, 5, "replica"),
+    "rows8k": ("8192x8192 synthetic RGB-D frame, M=5, row-tile sharded", 8192, 8192, 1, 5,
+               "rows"),
+}
+START_FRAME = 95  # timed frames cross scenario A's 1.5x illumination step at 100-112
+L2_BYTES = 126 * 2**20
+
+
+def bytes_per_px(mc: int, md: int) -> int:
+    """Algorithmic HBM bytes per pixel per frame of the fused kernel (SURVEY
+    8d): reads rgb 3 + depth 2 + colour state 4*(3+2)*Mc + depth state
+    4*(1+2)*Md + 2 init flags + fusion out/cpt 2; writes both states + 2."""
+    state = 4 * (5 * mc) + 4 * (3 * md)
+    return (3 + 2 + state + 2 + 2) + (state + 2)
+
+
+def load_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.lines, self.proc = gpu, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_reference(frames_host, width, height, mc, md, min_seconds=10.0, max_seconds=30.0,
+                  threads=None):
+    """Time the reference's own SequenceProcessor::process (compiled from
+    /root/reference sources into oracle/_ref) on host frames; falls back to
+    the C restatement if the reference build is absent."""
+    import oracle as O
+
+    threads = threads or os.cpu_count() or 1
+    npx = width * height
+    if O.ref_available():
+        ref = O.Ref()
+        proc = O.RefProcessor(ref, width, height, O.color_cfg(mc), O.depth_cfg(md),
+                              workers=threads)
+        run = lambda fr: proc.process(*fr, want_masks=False)  # noqa: E731
+        kind, cores = "reference", threads
+    else:
+        port = O.Port()
+        proc = O.PortProcessor(port, npx, O.color_cfg(mc), O.depth_cfg(md))
+        run = lambda fr: proc.process(*fr)  # noqa: E731
+        kind, cores = "port", 1
+    run(frames_host[0])  # initialisation frame, untimed
+    n, t0 = 0, time.perf_counter()
+    k = 1
+    while True:
+        run(frames_host[k % len(frames_host)])
+        k += 1
+        n += 1
+        dt = time.perf_counter() - t0
+        if (dt >= min_seconds and n >= len(frames_host) - 1) or dt >= max_seconds:
+            break
+    return {"value": npx * n / dt / 1e6, "unit": "Mpix/s", "cores": cores, "kind": kind,
+            "frames": n, "seconds": dt}
+
+
+def run_reference_arm(args):
+    """--impl reference: the reference CPU path on this host's cores, rank 0."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    name = args.workload
+    text, W, H, S, M, shard = WORKLOADS[name]
+    import oracle as O
+
+    # Each step: the next frame of `ref_streams` streams (a bounded sample of
+    # the workload), frames rendered by the oracle's C renderer (identical to
+    # the reference's render_frame) before timing.
+    ref_streams = min(S, args.ref_streams)
+    if W * H > 640 * 480 * 4:
+        ref_w, ref_h = W, min(H, max(1, (640 * 480 * 4) // W))  # a row band of the big frame
+    else:
+        ref_w, ref_h = W, H
+    port = O.Port()
+    scenes = [O.PortScene(port, "A", ref_w, ref_h, seed=s + 1) for s in range(ref_streams)]
+    nframes = args.warmup + args.steps
+    frames = [[(lambda fr: (fr.r, fr.g, fr.b, fr.depth))(sc.render(START_FRAME + f))
+               for sc in scenes] for f in range(nframes)]
+    threads = os.cpu_count() or 1
+    if O.ref_available():
+        ref = O.Ref()
+        procs = [O.RefProcessor(ref, ref_w, ref_h, O.color_cfg(M), O.depth_cfg(M),
+                                workers=threads) for _ in scenes]
+        kind = "reference"
+    else:
+        procs = [O.PortProcessor(port, ref_w * ref_h, O.color_cfg(M), O.depth_cfg(M))
+                 for _ in scenes]
+        kind, threads = "port", 1
+    for f in range(args.warmup):
+        for p, fr in zip(procs, frames[f]):
+            p.process(*fr)
+    t0 = time.perf_counter()
+    for f in range(args.warmup, nframes):
+        for p, fr in zip(procs, frames[f]):
+            p.process(*fr)
+    dt = time.perf_counter() - t0
+    px = ref_w * ref_h * ref_streams * args.steps
+    v = px / dt / 1e6
+    sample = (f"{ref_streams} stream(s) of {ref_w}x{ref_h} scenario A, frames "
+              f"{START_FRAME}..{START_FRAME + nframes - 1} ({args.warmup} warm-up), "
+              f"SequenceProcessor::process fused, workers={threads}")
+    print(json.dumps({
+        "impl": "reference", "metric": "RGB-D megapixels/s per GPU & box", "value": round(v, 3),
+        "unit": "Mpix/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "strong" if shard in ("stream", "rows") else "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
+        "config": {"workload": name, "description": text, "width": W, "height": H, "streams": S,
+                   "components": M},
+        "cpu_baseline": {"value": round(v, 3), "unit": "Mpix/s", "cores": threads, "kind": kind,
+                         "sample": sample},
+        "e2e": {"value": round(v, 3), "unit": "Mpix/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="streams256", choices=sorted(WORKLOADS))
+    ap.add_argument("--variant", default="auto", choices=["auto", "ldg", "ldg_elide"])
+    ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--ref-streams", type=int, default=4)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+
+    import paper_2110_14934_b200 as R
+    from paper_2110_14934_b200.shard import row_shard, stream_shard
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    def allmax(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    name = args.workload
+    text, W, H, S, M, shard = WORKLOADS[name]
+    # ---- this rank's shard -------------------------------------------------
+    if shard == "stream":
+        s0, s1 = stream_shard(S, rank, world)
+        my_streams, my_h, seed0, row0 = s1 - s0, H, 1 + s0, 0
+    elif shard == "rows":
+        y0, y1 = row_shard(H, rank, world)
+        my_streams, my_h, seed0, row0 = 1, y1 - y0, 1, y0
+    else:  # replica: one independent camera stream per GPU
+        my_streams, my_h, seed0, row0 = S, H, 1 + rank, 0
+    npx = W * my_h * my_streams
+    total_units = npx * (world if shard == "replica" else 1)
+
+    cfg = R.RunConfig.defaults()
+    cfg.color_gmm.components = cfg.depth_gmm.components = M
+    proc = R.SequenceProcessor(W, my_h, cfg, streams=my_streams, device=local,
+                               variant=args.variant)
+    ext = torch.cuda.ExternalStream(proc.stream_handle, device=dev)
+
+    # ---- inputs resident in HBM before timing --------------------------------
+    nframes = args.warmup + args.steps
+    frames = []
+    for f in range(nframes):
+        if shard == "rows":  # render the full-width frame's row band: render then slice
+            full = R.render_scenario("A", W, H, START_FRAME + f, streams=1, seed0=seed0,
+                                     device=local)
+            frames.append({k: v[:, row0:row0 + my_h].contiguous() for k, v in full.items()})
+            del full
+        else:
+            frames.append(R.render_scenario("A", W, H, START_FRAME + f, streams=my_streams,
+                                            seed0=seed0, device=local))
+    torch.cuda.synchronize()
+    state_bytes = npx * (bytes_per_px(M, M) - 5)
+    flush = state_bytes < 2 * L2_BYTES  # small working sets: flush L2 between steps
+    flush_buf = torch.empty(4 * L2_BYTES, dtype=torch.uint8, device=dev) if flush else None
+
+    def step(f):
+        fr = frames[f]
+        proc.submit(fr["r"], fr["g"], fr["b"], fr["depth"])
+
+    for f in range(args.warmup):
+        step(f)
+    # ---- timed region: kernel-only, frames in HBM ----------------------------
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    barrier()
+    launches0 = R.launch_count()
+    with ClockSampler(local) as clk:
+        region0 = torch.cuda.Event(enable_timing=True)
+        region1 = torch.cuda.Event(enable_timing=True)
+        region0.record(ext)
+        for k in range(args.steps):
+            if flush:
+                with torch.cuda.stream(ext):
+                    flush_buf.fill_(k & 0xFF)
+            starts[k].record(ext)
+            step(args.warmup + k)
+            ends[k].record(ext)
+        region1.record(ext)
+        proc.sync()
+        barrier()
+    launches = R.launch_count() - launches0
+    kernel_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    region_ms = region0.elapsed_time(region1)
+    busy_ms = sum(kernel_ms) if flush else region_ms
+    busy_ms = allmax(busy_ms)
+    ms_per_step = busy_ms / args.steps
+    value = total_units * args.steps / (busy_ms / 1e3) / 1e6
+
+    # ---- roofline of the fused kernel ----------------------------------------
+    peak, peak_src = load_peak()
+    bpp = bytes_per_px(M, M)
+    launch_ms = float(np.mean(kernel_ms))  # one fused launch per step on this rank
+    achieved = bpp * npx / (launch_ms / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        try:
+            tr = json.load(open(tp)).get(f"{name}:{args.variant}:{world}")
+            traffic = tr
+        except Exception:
+            traffic = None
+
+    # ---- e2e: public API, pinned host frames in, fused masks out --------------
+    e2e_steps = args.e2e_steps or args.steps
+    host = []
+    for f in range(2):  # a ring of two distinct pinned host frame sets
+        hf = {}
+        for k in ("r", "g", "b", "depth"):
+            src = frames[args.warmup + f][k]
+            t = torch.empty(src.shape, dtype=src.dtype, pin_memory=True)
+            if src.dtype == torch.uint16:  # copy through int16 views (raw bytes)
+                t.view(torch.int16).copy_(src.view(torch.int16))
+            else:
+                t.copy_(src)
+            hf[k] = t
+        host.append(hf)
+    outs = [torch.empty((my_streams, my_h, W), dtype=torch.uint8, pin_memory=True)
+            for _ in range(2)]
+    torch.cuda.synchronize()
+
+    def as_np(t):
+        return t.view(torch.int16).numpy().view(np.uint16) if t.dtype == torch.uint16 \
+            else t.numpy()
+
+    host_np = [{k: as_np(v) for k, v in hf.items()} for hf in host]
+    outs_np = [o.numpy() for o in outs]
+    for k in range(2):  # warm the host path
+        hf = host_np[k % 2]
+        proc.submit(hf["r"], hf["g"], hf["b"], hf["depth"], fused=outs_np[k % 2])
+    proc.sync()
+    barrier()
+    t0 = time.perf_counter()
+    for k in range(e2e_steps):
+        hf = host_np[k % 2]
+        proc.submit(hf["r"], hf["g"], hf["b"], hf["depth"], fused=outs_np[k % 2])
+    proc.sync()
+    barrier()
+    e2e_s = allmax(time.perf_counter() - t0)
+    e2e_value = total_units * e2e_steps / e2e_s / 1e6
+    # synchronous reference-semantics call (process() per frame, no overlap)
+    barrier()
+    t0 = time.perf_counter()
+    for k in range(min(e2e_steps, 5)):
+        hf = host_np[k % 2]
+        proc.process(hf["r"], hf["g"], hf["b"], hf["depth"], want=(),
+                     out={"fused": outs_np[k % 2]})
+    sync_s = allmax(time.perf_counter() - t0)
+    sync_value = total_units * min(e2e_steps, 5) / sync_s / 1e6
+
+    # ---- CPU baseline (rank 0, N=1 only) -------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sample_frames = []
+        for f in range(min(nframes, 8)):
+            fr = frames[f]
+            sample_frames.append(tuple(
+                (fr[k][0].view(torch.int16).cpu().numpy().view(np.uint16)
+                 if fr[k].dtype == torch.uint16 else fr[k][0].cpu().numpy())
+                for k in ("r", "g", "b", "depth")))
+        cb = cpu_reference(sample_frames, W, my_h, M, M, min_seconds=args.cpu_seconds)
+        cpu = {"value": round(cb["value"], 3), "unit": "Mpix/s", "cores": cb["cores"],
+               "kind": cb["kind"],
+               "sample": (f"stream 0 ({W}x{my_h}, seed {seed0}) frames {START_FRAME}.."
+                          f"{START_FRAME + len(sample_frames) - 1} cycled, {cb['frames']} "
+                          f"frames in {cb['seconds']:.1f} s, SequenceProcessor::process "
+                          f"(fused), workers={cb['cores']}")}
+
+    if rank == 0:
+        line = {
+            "metric": "RGB-D megapixels/s per GPU & box",
+            "value": round(value, 2),
+            "unit": "Mpix/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(ms_per_step, 4),
+            "higher_is_better": True,
+            "scaling": "strong" if shard in ("stream", "rows") else "weak",
+            "vs_baseline": None,
+            "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": name, "description": text, "width": W, "height": H,
+                       "streams": S, "components_color": M, "components_depth": M,
+                       "scenario": "A", "frames": f"{START_FRAME}..{START_FRAME + nframes - 1}",
+                       "pixels_per_step": total_units, "variant": args.variant,
+                       "parallelism": f"{shard}-sharded x{world}",
+                       "l2": ("flushed between steps (4x L2 buffer), per-step kernel events summed"
+                              if flush else "working set larger than L2 (no flush)")},
+            "per_gpu_value": round(value / world, 2),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "algorithmic_bytes_per_px": bpp, "peak_source": peak_src,
+                         "kernel_ms": round(launch_ms, 4)},
+            "cpu_baseline": cpu,
+            "e2e": {"value": round(e2e_value, 2), "unit": "Mpix/s",
+                    "h2d_bytes_per_step": 5 * npx, "d2h_bytes_per_step": npx,
+                    "mode": "submit/sync pipelined, pinned host frames",
+                    "sync_process_value": round(sync_value, 2)},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,188 @@
+/*
+ * rgbdseg_c.h -- C-ABI of the B200-native rgbdseg hot path.
+ *
+ * Drop-in boundary for the reference library's model/segment API
+ * (/root/reference/proj/include/rgbdseg/*.hpp).  Plain pointers and sizes
+ * only; no C++ or torch types.  Every entry point names the reference
+ * interface it replaces.  The library (librgbdseg_b200.so) owns all device
+ * memory; callers own host buffers.
+ *
+ * Memory: every frame/mask pointer may be host memory (pageable or pinned) or
+ * device memory of the handle's GPU; the library classifies each pointer with
+ * cudaPointerGetAttributes and moves data accordingly.
+ *
+ * Errors: functions return an rgbdseg_status; rgbdseg_last_error() returns a
+ * thread-local message for the last failing call on this thread.
+ *   RGBDSEG_EINVAL  <-> std::invalid_argument in the reference (bad config,
+ *                       dimension or mode mismatch: plane.hpp:53-58,
+ *                       mixture.cpp:9-24, segmenter.cpp:74-75,109-125,
+ *                       fusion.cpp:8-9)
+ *   RGBDSEG_ECUDA / ENOMEM / ERUNTIME  <-> std::runtime_error
+ *
+ * Threading: a handle is not thread-safe (the reference banks/processors are
+ * not either, processor.hpp:57-59).  Handles on different GPUs are independent.
+ */
+#ifndef RGBDSEG_C_H
+#define RGBDSEG_C_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    RGBDSEG_OK = 0,
+    RGBDSEG_EINVAL = 1,
+    RGBDSEG_ECUDA = 2,
+    RGBDSEG_ENOMEM = 3,
+    RGBDSEG_ERUNTIME = 4
+} rgbdseg_status;
+
+/* Bank modes, segmenter.hpp:11 (Augmented4 is not on this path). */
+enum { RGBDSEG_COLOR3 = 0, RGBDSEG_DEPTH1 = 1 };
+
+/* MixtureConfig, mixture.hpp:16-26 -- same fields, same order, same defaults
+ * (rgbdseg_mixture_defaults). */
+typedef struct rgbdseg_mixture_cfg {
+    int components;             /* M in [3,5] */
+    float learning_rate;        /* alpha in (0,1) */
+    float match_lambda;         /* lambda > 0 */
+    float background_threshold; /* T in (0,1) */
+    float initial_sigma;        /* sigma_0 > 0 */
+    float initial_weight;       /* w_new in (0,1) */
+    float variance_floor;       /* > 0 */
+} rgbdseg_mixture_cfg;
+
+/* PixelMixture, mixture.hpp:30-41: means[i*channels + c]. */
+typedef struct rgbdseg_pixel_mixture {
+    int components;
+    int channels;
+    float means[20];
+    float variances[5];
+    float weights[5];
+} rgbdseg_pixel_mixture;
+
+typedef struct rgbdseg_bank rgbdseg_bank;
+typedef struct rgbdseg_fusion rgbdseg_fusion;
+typedef struct rgbdseg_processor rgbdseg_processor;
+
+/* ---- library ---------------------------------------------------------- */
+const char* rgbdseg_last_error(void);
+const char* rgbdseg_version(void);
+/* Number of kernel launches this process has issued through the library. */
+uint64_t rgbdseg_launch_count(void);
+
+/* ---- config: MixtureConfig::validate, mixture.cpp:9-24 ----------------- */
+void rgbdseg_mixture_defaults(rgbdseg_mixture_cfg* out); /* mixture.hpp:17-23 */
+int rgbdseg_mixture_validate(const rgbdseg_mixture_cfg* cfg);
+
+/* ---- per-pixel API: mixture.hpp:43-60, run on the GPU ------------------
+ * Batched over n independent records (AoS, host or device memory).
+ * init: values[n*channels] -> out[n]                (init_mixture)
+ * step: mix[n] updated in place, labels[n] 1=FG      (step_pixel); like
+ *       the reference, step uses each record's own `components` for the
+ *       loops and cfg only for the rates; every record must have
+ *       `channels` channels and 3..5 components, else RGBDSEG_EINVAL.    */
+int rgbdseg_init_mixtures(const float* values, int channels, size_t n,
+                          const rgbdseg_mixture_cfg* cfg, rgbdseg_pixel_mixture* out,
+                          int device);
+int rgbdseg_step_mixtures(rgbdseg_pixel_mixture* mix, const float* values, int channels,
+                          size_t n, const rgbdseg_mixture_cfg* cfg, uint8_t* labels, int device);
+
+/* ---- ModelBank: segmenter.hpp:25-55 ------------------------------------
+ * Device-resident SoA bank over `npx` = width*height*streams pixels.
+ * Plane ids (ModelBank plane order, segmenter.hpp:51-54):
+ *   mean(i,c) = i*C + c ; variance(i) = M*C + i ; weight(i) = M*C + M + i ;
+ *   the initialised-flag plane (uint8) is plane id RGBDSEG_FLAGS_PLANE.   */
+#define RGBDSEG_FLAGS_PLANE (-1)
+int rgbdseg_bank_create(int width, int height, int streams, int mode,
+                        const rgbdseg_mixture_cfg* cfg, int device, rgbdseg_bank** out);
+void rgbdseg_bank_destroy(rgbdseg_bank* bank);
+int rgbdseg_bank_planes(const rgbdseg_bank* bank); /* M*C + 2M */
+/* Copy one plane (npx elements; float, or uint8 for the flag plane) out of /
+ * into the bank.  Backs gather/scatter/mean_plane/state_equals. */
+int rgbdseg_bank_download(const rgbdseg_bank* bank, int plane, void* dst);
+int rgbdseg_bank_upload(rgbdseg_bank* bank, int plane, const void* src);
+/* Device base pointer of the state planes / the flag plane, and the plane
+ * pitch in elements (>= npx, padded for 128-byte alignment). */
+int rgbdseg_bank_device_ptrs(const rgbdseg_bank* bank, float** state, uint8_t** flags,
+                             size_t* pitch);
+
+/* segment_color, segmenter.cpp:107-119 / segment_depth, :121-131.
+ * Planes are npx elements, row-major, streams back to back.  mask_out may be
+ * NULL (state update only).  Synchronous like the reference. */
+int rgbdseg_segment_color(rgbdseg_bank* bank, const uint8_t* r, const uint8_t* g,
+                          const uint8_t* b, const rgbdseg_mixture_cfg* cfg, uint8_t* mask_out);
+int rgbdseg_segment_depth(rgbdseg_bank* bank, const uint16_t* depth_mm,
+                          const rgbdseg_mixture_cfg* cfg, uint8_t* mask_out);
+
+/* ---- FusionState / reset_state / fuse_step: fusion.hpp:11-23 ----------- */
+int rgbdseg_fusion_create(int width, int height, int streams, int initial_label,
+                          int counter_limit, int device, rgbdseg_fusion** out);
+void rgbdseg_fusion_destroy(rgbdseg_fusion* fs);
+/* out_copy (may be NULL) receives the fused mask (= state.out). */
+int rgbdseg_fusion_step(rgbdseg_fusion* fs, const uint8_t* rgb_mask, const uint8_t* depth_mask,
+                        uint8_t* out_copy);
+int rgbdseg_fusion_download(const rgbdseg_fusion* fs, uint8_t* out, int8_t* cpt);
+int rgbdseg_fusion_upload(rgbdseg_fusion* fs, const uint8_t* out, const int8_t* cpt);
+
+/* ---- SequenceProcessor: processor.hpp:60-80, process = processor.cpp:158-184
+ * Fused method on a registered sequence: colour bank + depth bank + List-1
+ * fusion, executed as ONE kernel per frame batch over `streams` independent
+ * camera streams of width x height (state never leaves HBM, masks never
+ * round-trip HBM).                                                        */
+typedef struct rgbdseg_processor_cfg {
+    int width, height;
+    int streams;           /* independent camera streams batched per step */
+    rgbdseg_mixture_cfg color;
+    rgbdseg_mixture_cfg depth;
+    int fusion_counter_limit; /* >= 1 (fusion.cpp:8); <= 127, cpt is int8 */
+    int fusion_initial_label; /* 0 or 1 */
+    int device;
+    int host_chunks;       /* 0 = auto: H2D/compute/D2H overlap chunks for host frames */
+} rgbdseg_processor_cfg;
+
+void rgbdseg_processor_defaults(rgbdseg_processor_cfg* cfg, int width, int height);
+int rgbdseg_processor_create(const rgbdseg_processor_cfg* cfg, rgbdseg_processor** out);
+void rgbdseg_processor_destroy(rgbdseg_processor* p);
+
+/* One frame step for all streams.  Inputs: r, g, b (uint8) and depth (uint16,
+ * raw millimetres, 0 = no return), npx elements each, host or device.
+ * Outputs (any may be NULL): fused mask, colour mask, depth mask.
+ * rgbdseg_processor_process is synchronous (reference semantics);
+ * rgbdseg_processor_submit only enqueues -- buffers must stay valid until
+ * rgbdseg_processor_sync returns. */
+int rgbdseg_processor_process(rgbdseg_processor* p, const uint8_t* r, const uint8_t* g,
+                              const uint8_t* b, const uint16_t* depth, uint8_t* fused_out,
+                              uint8_t* rgb_out, uint8_t* depth_out);
+int rgbdseg_processor_submit(rgbdseg_processor* p, const uint8_t* r, const uint8_t* g,
+                             const uint8_t* b, const uint16_t* depth, uint8_t* fused_out,
+                             uint8_t* rgb_out, uint8_t* depth_out);
+int rgbdseg_processor_sync(rgbdseg_processor* p);
+int64_t rgbdseg_processor_frames(const rgbdseg_processor* p);
+/* Borrow the processor's banks / fusion state (owned by the processor):
+ * color_bank()/depth_bank(), processor.hpp:67-68. */
+rgbdseg_bank* rgbdseg_processor_color_bank(rgbdseg_processor* p);
+rgbdseg_bank* rgbdseg_processor_depth_bank(rgbdseg_processor* p);
+rgbdseg_fusion* rgbdseg_processor_fusion(rgbdseg_processor* p);
+/* The CUDA stream the processor's kernels run on (cudaStream_t as void*),
+ * so callers can time the kernels with events on the launching stream. */
+void* rgbdseg_processor_stream(rgbdseg_processor* p);
+/* Kernel variant: 0 = auto, 1 = LDG one pixel per thread, 2 = TMA bulk. */
+int rgbdseg_processor_set_variant(rgbdseg_processor* p, int variant);
+
+/* ---- synthetic scenes on the GPU (synthetic.cpp:119-195, harness) ------
+ * Renders builtin scenario `name` ('A' or 'B'), frame `frame`, for `streams`
+ * streams whose seeds are seed0 + s, directly into device planes (npx each).
+ * Scenario geometry is the builtin 640x480 one unless width/height differ,
+ * in which case events and the object keep their builtin pixel coordinates. */
+int rgbdseg_render_scenario(char name, int width, int height, int streams, uint64_t seed0,
+                            int frame, uint8_t* r, uint8_t* g, uint8_t* b, uint16_t* depth,
+                            uint8_t* gt, int device, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RGBDSEG_C_H */

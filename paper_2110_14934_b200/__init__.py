@@ -1,0 +1,29 @@
+"""B200-native (sm_100a) RGB-D Gaussian-mixture background model + List-1
+colour/depth mask fusion -- the hot path of arXiv 2110.14934's reference
+library ``rgbdseg``, rebuilt as hand-written CUDA behind the reference's own
+model/segment API.  See DESIGN.md."""
+from ._lib import launch_count  # noqa: F401  (fails loudly without the CUDA library)
+from .rgbdseg import (  # noqa: F401
+    PIXEL_MIXTURE_DTYPE,
+    BankMode,
+    FrameMasks,
+    FusionState,
+    MixtureConfig,
+    ModelBank,
+    PixelMixture,
+    RunConfig,
+    SequenceProcessor,
+    builtin_scenario_names,
+    default_config_json,
+    fuse_step,
+    init_mixture,
+    init_mixtures,
+    render_scenario,
+    reset_state,
+    segment_color,
+    segment_depth,
+    step_mixtures,
+    step_pixel,
+)
+
+__all__ = [n for n in dir() if not n.startswith("_")]

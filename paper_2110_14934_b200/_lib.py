@@ -1,0 +1,133 @@
+"""ctypes binding of librgbdseg_b200.so (include/rgbdseg_c.h).
+
+The product path has no CPU fallback: if the CUDA library is missing this
+module raises at import time, and every compute call goes through the C-ABI
+into the sm_100a kernels.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("RGBDSEG_B200_LIB", os.path.join(HERE, "librgbdseg_b200.so"))
+
+OK, EINVAL, ECUDA, ENOMEM, ERUNTIME = 0, 1, 2, 3, 4
+COLOR3, DEPTH1 = 0, 1
+FLAGS_PLANE = -1
+VARIANTS = {"auto": 0, "ldg": 1, "ldg_elide": 2, "bulk": 3}
+
+
+class MixtureCfg(C.Structure):
+    _fields_ = [
+        ("components", C.c_int),
+        ("learning_rate", C.c_float),
+        ("match_lambda", C.c_float),
+        ("background_threshold", C.c_float),
+        ("initial_sigma", C.c_float),
+        ("initial_weight", C.c_float),
+        ("variance_floor", C.c_float),
+    ]
+
+
+class PixelMixtureRec(C.Structure):
+    _fields_ = [
+        ("components", C.c_int),
+        ("channels", C.c_int),
+        ("means", C.c_float * 20),
+        ("variances", C.c_float * 5),
+        ("weights", C.c_float * 5),
+    ]
+
+
+class ProcessorCfg(C.Structure):
+    _fields_ = [
+        ("width", C.c_int),
+        ("height", C.c_int),
+        ("streams", C.c_int),
+        ("color", MixtureCfg),
+        ("depth", MixtureCfg),
+        ("fusion_counter_limit", C.c_int),
+        ("fusion_initial_label", C.c_int),
+        ("device", C.c_int),
+        ("host_chunks", C.c_int),
+    ]
+
+
+# Every symbol include/rgbdseg_c.h declares: (restype, argtypes)
+_vp, _sz, _i, _u8 = C.c_void_p, C.c_size_t, C.c_int, C.c_uint8
+SIGNATURES = {
+    "rgbdseg_last_error": (C.c_char_p, []),
+    "rgbdseg_version": (C.c_char_p, []),
+    "rgbdseg_launch_count": (C.c_uint64, []),
+    "rgbdseg_mixture_defaults": (None, [C.POINTER(MixtureCfg)]),
+    "rgbdseg_mixture_validate": (_i, [C.POINTER(MixtureCfg)]),
+    "rgbdseg_init_mixtures": (_i, [_vp, _i, _sz, C.POINTER(MixtureCfg), _vp, _i]),
+    "rgbdseg_step_mixtures": (_i, [_vp, _vp, _i, _sz, C.POINTER(MixtureCfg), _vp, _i]),
+    "rgbdseg_bank_create": (_i, [_i, _i, _i, _i, C.POINTER(MixtureCfg), _i, C.POINTER(_vp)]),
+    "rgbdseg_bank_destroy": (None, [_vp]),
+    "rgbdseg_bank_planes": (_i, [_vp]),
+    "rgbdseg_bank_download": (_i, [_vp, _i, _vp]),
+    "rgbdseg_bank_upload": (_i, [_vp, _i, _vp]),
+    "rgbdseg_bank_device_ptrs": (_i, [_vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_sz)]),
+    "rgbdseg_segment_color": (_i, [_vp, _vp, _vp, _vp, C.POINTER(MixtureCfg), _vp]),
+    "rgbdseg_segment_depth": (_i, [_vp, _vp, C.POINTER(MixtureCfg), _vp]),
+    "rgbdseg_fusion_create": (_i, [_i, _i, _i, _i, _i, _i, C.POINTER(_vp)]),
+    "rgbdseg_fusion_destroy": (None, [_vp]),
+    "rgbdseg_fusion_step": (_i, [_vp, _vp, _vp, _vp]),
+    "rgbdseg_fusion_download": (_i, [_vp, _vp, _vp]),
+    "rgbdseg_fusion_upload": (_i, [_vp, _vp, _vp]),
+    "rgbdseg_processor_defaults": (None, [C.POINTER(ProcessorCfg), _i, _i]),
+    "rgbdseg_processor_create": (_i, [C.POINTER(ProcessorCfg), C.POINTER(_vp)]),
+    "rgbdseg_processor_destroy": (None, [_vp]),
+    "rgbdseg_processor_process": (_i, [_vp] * 8),
+    "rgbdseg_processor_submit": (_i, [_vp] * 8),
+    "rgbdseg_processor_sync": (_i, [_vp]),
+    "rgbdseg_processor_frames": (C.c_int64, [_vp]),
+    "rgbdseg_processor_color_bank": (_vp, [_vp]),
+    "rgbdseg_processor_depth_bank": (_vp, [_vp]),
+    "rgbdseg_processor_fusion": (_vp, [_vp]),
+    "rgbdseg_processor_stream": (_vp, [_vp]),
+    "rgbdseg_processor_set_variant": (_i, [_vp, _i]),
+    "rgbdseg_render_scenario": (_i, [C.c_char, _i, _i, _i, C.c_uint64, _i, _vp, _vp, _vp, _vp,
+                                     _vp, _i, _vp]),
+}
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: the B200 CUDA library is not built "
+            "(run `make lib` or __graft_entry__.build()); there is no CPU fallback")
+    lib = C.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+lib = _load()
+
+
+class RgbdsegError(RuntimeError):
+    pass
+
+
+def check(rc: int, what: str = ""):
+    """Map a C-ABI status to the reference's exception types:
+    EINVAL -> ValueError (std::invalid_argument), others -> RuntimeError."""
+    if rc == OK:
+        return
+    msg = (lib.rgbdseg_last_error() or b"").decode()
+    if what:
+        msg = f"{what}: {msg}"
+    if rc == EINVAL:
+        raise ValueError(msg)
+    if rc == ENOMEM:
+        raise MemoryError(msg)
+    raise RgbdsegError(msg)
+
+
+def launch_count() -> int:
+    return int(lib.rgbdseg_launch_count())

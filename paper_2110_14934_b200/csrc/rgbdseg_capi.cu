@@ -1,0 +1,803 @@
+// rgbdseg_capi.cu -- C-ABI host runtime (include/rgbdseg_c.h).
+//
+// Owns device memory, CUDA streams and events for banks, fusion states and
+// processors, and drives the sm_100a kernels in rgbdseg_kernels.cu.  The
+// reference's executor (parallel_for_rows, engine.cpp:14-37) becomes the CUDA
+// grid; its 3-stage ingest/process/emit pipeline (run_pipeline,
+// engine.hpp:54-139) becomes H2D / kernel / D2H on three CUDA streams chained
+// by events, double-buffered over pixel chunks of a frame and across frames.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/rgbdseg_c.h"
+#include "rgbdseg_kernels.cuh"
+
+using namespace rgbdseg_b200;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    return fail(e == cudaErrorMemoryAllocation ? RGBDSEG_ENOMEM : RGBDSEG_ECUDA,
+                std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CU(call)                                                   \
+    do {                                                           \
+        cudaError_t e_ = (call);                                   \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call);        \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = 0;
+    bool ok = false;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) == cudaSuccess && cudaSetDevice(dev) == cudaSuccess) ok = true;
+    }
+    ~DeviceGuard() {
+        if (ok) cudaSetDevice(prev);
+    }
+};
+
+#define GUARD(dev)                                                              \
+    DeviceGuard guard_(dev);                                                    \
+    if (!guard_.ok) return cuda_fail(cudaGetLastError(), "cudaSetDevice")
+
+// MixtureConfig::validate, mixture.cpp:9-24 (same messages).
+int validate_cfg(const rgbdseg_mixture_cfg* c) {
+    if (!c) return fail(RGBDSEG_EINVAL, "MixtureConfig: null");
+    if (c->components < 3 || c->components > 5)
+        return fail(RGBDSEG_EINVAL, "MixtureConfig: components must be in [3,5]");
+    if (!(c->learning_rate > 0.0f && c->learning_rate < 1.0f))
+        return fail(RGBDSEG_EINVAL, "MixtureConfig: learning_rate must be in (0,1)");
+    if (!(c->background_threshold > 0.0f && c->background_threshold < 1.0f))
+        return fail(RGBDSEG_EINVAL, "MixtureConfig: background_threshold must be in (0,1)");
+    if (!(c->match_lambda > 0.0f))
+        return fail(RGBDSEG_EINVAL, "MixtureConfig: match_lambda must be positive");
+    if (!(c->initial_sigma > 0.0f))
+        return fail(RGBDSEG_EINVAL, "MixtureConfig: initial_sigma must be positive");
+    if (!(c->initial_weight > 0.0f && c->initial_weight < 1.0f))
+        return fail(RGBDSEG_EINVAL, "MixtureConfig: initial_weight must be in (0,1)");
+    if (!(c->variance_floor > 0.0f))
+        return fail(RGBDSEG_EINVAL, "MixtureConfig: variance_floor must be positive");
+    return RGBDSEG_OK;
+}
+
+MixCfg to_k(const rgbdseg_mixture_cfg& c) {
+    return MixCfg{c.learning_rate,  c.match_lambda,   c.background_threshold,
+                  c.initial_sigma, c.initial_weight, c.variance_floor};
+}
+
+bool on_device(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+size_t pitch_for(size_t npx) { return (npx + 63) & ~size_t(63); }  // 256-byte planes
+
+int check_dims(int w, int h, int streams) {
+    if (w <= 0 || h <= 0) return fail(RGBDSEG_EINVAL, "Plane: non-positive dimensions");
+    if (streams <= 0) return fail(RGBDSEG_EINVAL, "streams must be positive");
+    return RGBDSEG_OK;
+}
+
+template <typename T>
+int dalloc(T** p, size_t n) {
+    *p = nullptr;
+    if (n == 0) return RGBDSEG_OK;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T));
+    if (e != cudaSuccess) {
+        *p = nullptr;
+        return cuda_fail(e, "cudaMalloc");
+    }
+    return RGBDSEG_OK;
+}
+
+template <typename T>
+void dfree(T*& p) {
+    if (p) cudaFree(p);
+    p = nullptr;
+}
+
+// Scratch device buffer that grows on demand.
+struct Scratch {
+    void* p = nullptr;
+    size_t bytes = 0;
+    int get(size_t want, void** out) {
+        if (want > bytes) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            bytes = 0;
+            cudaError_t e = cudaMalloc(&p, want);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(scratch)");
+            bytes = want;
+        }
+        *out = p;
+        return RGBDSEG_OK;
+    }
+    ~Scratch() {
+        if (p) cudaFree(p);
+    }
+};
+
+// Stage `bytes` of a host-or-device source into device memory: device
+// pointers are used in place, host pointers are copied into `scratch`.
+int stage_in(const void* src, size_t bytes, Scratch& scratch, const void** dev, cudaStream_t s) {
+    if (on_device(src)) {
+        *dev = src;
+        return RGBDSEG_OK;
+    }
+    void* d;
+    if (int rc = scratch.get(bytes, &d)) return rc;
+    CU(cudaMemcpyAsync(d, src, bytes, cudaMemcpyDefault, s));
+    *dev = d;
+    return RGBDSEG_OK;
+}
+
+}  // namespace
+
+// ============================================================== handles
+struct rgbdseg_bank {
+    int width, height, streams, mode, M, C, device;
+    size_t npx, pitch;
+    rgbdseg_mixture_cfg cfg;
+    float* state = nullptr;
+    uint8_t* flags = nullptr;
+    cudaStream_t stream = nullptr;
+    Scratch s_r, s_g, s_b, s_mask;
+    BankView view() const { return BankView{state, flags, pitch, M, C}; }
+};
+
+struct rgbdseg_fusion {
+    size_t npx;
+    int limit, device;
+    uint8_t* out = nullptr;
+    int8_t* cpt = nullptr;
+    cudaStream_t stream = nullptr;
+    Scratch s_rgb, s_dep;
+};
+
+struct Slot {
+    uint8_t *r = nullptr, *g = nullptr, *b = nullptr;
+    uint16_t* d = nullptr;
+    uint8_t *rgbm = nullptr, *depm = nullptr;
+    cudaEvent_t h2d_done = nullptr, k_done = nullptr, d2h_done = nullptr;
+};
+
+struct rgbdseg_processor {
+    rgbdseg_processor_cfg cfg;
+    rgbdseg_bank* color = nullptr;
+    rgbdseg_bank* depth = nullptr;
+    rgbdseg_fusion* fusion = nullptr;
+    cudaStream_t sc = nullptr, sh2d = nullptr, sd2h = nullptr;
+    size_t npx = 0, chunk = 0;
+    int nchunks = 1;
+    Slot slot[2];
+    std::vector<cudaEvent_t> chunk_d2h;  // per chunk: last D2H reading fusion.out of it
+    uint64_t seq = 0;
+    int64_t frames = 0;
+    int variant = kAuto;
+};
+
+extern "C" {
+
+const char* rgbdseg_last_error(void) { return g_err.c_str(); }
+const char* rgbdseg_version(void) { return "rgbdseg-b200 0.1 (sm_100a)"; }
+uint64_t rgbdseg_launch_count(void) { return launches(); }
+
+void rgbdseg_mixture_defaults(rgbdseg_mixture_cfg* out) {
+    *out = rgbdseg_mixture_cfg{3, 0.05f, 2.5f, 0.8f, 15.0f, 0.05f, 4.0f};
+}
+
+int rgbdseg_mixture_validate(const rgbdseg_mixture_cfg* cfg) { return validate_cfg(cfg); }
+
+// ------------------------------------------------------------ per pixel
+int rgbdseg_init_mixtures(const float* values, int channels, size_t n,
+                          const rgbdseg_mixture_cfg* cfg, rgbdseg_pixel_mixture* out,
+                          int device) {
+    if (int rc = validate_cfg(cfg)) return rc;  // init_mixture validates (mixture.cpp:59)
+    if (channels < 1 || channels > 4)
+        return fail(RGBDSEG_EINVAL, "init_mixture: bad observation dimensionality");
+    if (n == 0) return RGBDSEG_OK;
+    GUARD(device);
+    float* dv;
+    PixRec* dr;
+    if (int rc = dalloc(&dv, n * channels)) return rc;
+    if (int rc = dalloc(&dr, n)) {
+        dfree(dv);
+        return rc;
+    }
+    cudaError_t e = cudaMemcpy(dv, values, n * channels * sizeof(float), cudaMemcpyDefault);
+    if (e == cudaSuccess) e = launch_mix_init(dv, channels, n, to_k(*cfg), cfg->components, dr, 0);
+    if (e == cudaSuccess) e = cudaMemcpy(out, dr, n * sizeof(PixRec), cudaMemcpyDefault);
+    dfree(dv);
+    dfree(dr);
+    if (e != cudaSuccess) return cuda_fail(e, "init_mixtures");
+    return RGBDSEG_OK;
+}
+
+int rgbdseg_step_mixtures(rgbdseg_pixel_mixture* mix, const float* values, int channels,
+                          size_t n, const rgbdseg_mixture_cfg* cfg, uint8_t* labels, int device) {
+    static_assert(sizeof(PixRec) == sizeof(rgbdseg_pixel_mixture), "record layout");
+    if (!cfg) return fail(RGBDSEG_EINVAL, "step_pixel: null config");
+    if (channels < 1 || channels > 4)
+        return fail(RGBDSEG_EINVAL, "step_pixel: bad observation dimensionality");
+    if (n == 0) return RGBDSEG_OK;
+    GUARD(device);
+    float* dv;
+    PixRec* dr;
+    uint8_t* dl;
+    if (int rc = dalloc(&dv, n * channels)) return rc;
+    if (int rc = dalloc(&dr, n)) {
+        dfree(dv);
+        return rc;
+    }
+    if (int rc = dalloc(&dl, n)) {
+        dfree(dv);
+        dfree(dr);
+        return rc;
+    }
+    std::vector<uint8_t> hl(n);
+    cudaError_t e = cudaMemcpy(dv, values, n * channels * sizeof(float), cudaMemcpyDefault);
+    if (e == cudaSuccess) e = cudaMemcpy(dr, mix, n * sizeof(PixRec), cudaMemcpyDefault);
+    if (e == cudaSuccess)
+        e = launch_mix_step(dr, dv, channels, n, to_k(*cfg), dl, 0);
+    if (e == cudaSuccess) e = cudaMemcpy(mix, dr, n * sizeof(PixRec), cudaMemcpyDefault);
+    if (e == cudaSuccess) e = cudaMemcpy(hl.data(), dl, n, cudaMemcpyDeviceToHost);
+    dfree(dv);
+    dfree(dr);
+    dfree(dl);
+    if (e != cudaSuccess) return cuda_fail(e, "step_mixtures");
+    for (size_t i = 0; i < n; ++i)
+        if (hl[i] == 255)
+            return fail(RGBDSEG_EINVAL,
+                        "step_pixel: record " + std::to_string(i) +
+                            " has components outside [3,5] or a channel-count mismatch");
+    if (labels) {
+        if (on_device(labels)) {
+            CU(cudaMemcpy(labels, hl.data(), n, cudaMemcpyHostToDevice));
+        } else {
+            std::memcpy(labels, hl.data(), n);
+        }
+    }
+    return RGBDSEG_OK;
+}
+
+// ------------------------------------------------------------ banks
+int rgbdseg_bank_create(int width, int height, int streams, int mode,
+                        const rgbdseg_mixture_cfg* cfg, int device, rgbdseg_bank** out) {
+    *out = nullptr;
+    if (int rc = check_dims(width, height, streams)) return rc;
+    if (mode != RGBDSEG_COLOR3 && mode != RGBDSEG_DEPTH1)
+        return fail(RGBDSEG_EINVAL, "unknown bank mode");
+    if (int rc = validate_cfg(cfg)) return rc;  // segmenter.cpp:26
+    GUARD(device);
+    auto* b = new rgbdseg_bank();
+    b->width = width;
+    b->height = height;
+    b->streams = streams;
+    b->mode = mode;
+    b->M = cfg->components;
+    b->C = mode == RGBDSEG_COLOR3 ? 3 : 1;
+    b->device = device;
+    b->cfg = *cfg;
+    b->npx = (size_t)width * height * streams;
+    b->pitch = pitch_for(b->npx);
+    const size_t planes = (size_t)b->M * b->C + 2 * b->M;
+    int rc = dalloc(&b->state, planes * b->pitch);
+    if (!rc) rc = dalloc(&b->flags, b->pitch);
+    if (!rc) {
+        cudaError_t e = cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = launch_bank_reset(b->view(), cfg->initial_sigma, b->npx, b->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(b->stream);
+        if (e != cudaSuccess) rc = cuda_fail(e, "bank_create");
+    }
+    if (rc) {
+        rgbdseg_bank_destroy(b);
+        return rc;
+    }
+    *out = b;
+    return RGBDSEG_OK;
+}
+
+void rgbdseg_bank_destroy(rgbdseg_bank* b) {
+    if (!b) return;
+    DeviceGuard g(b->device);
+    if (b->stream) cudaStreamSynchronize(b->stream);
+    dfree(b->state);
+    dfree(b->flags);
+    if (b->stream) cudaStreamDestroy(b->stream);
+    delete b;
+}
+
+int rgbdseg_bank_planes(const rgbdseg_bank* b) { return b->M * b->C + 2 * b->M; }
+
+int rgbdseg_bank_device_ptrs(const rgbdseg_bank* b, float** state, uint8_t** flags,
+                             size_t* pitch) {
+    if (state) *state = b->state;
+    if (flags) *flags = b->flags;
+    if (pitch) *pitch = b->pitch;
+    return RGBDSEG_OK;
+}
+
+int rgbdseg_bank_download(const rgbdseg_bank* b, int plane, void* dst) {
+    GUARD(b->device);
+    CU(cudaStreamSynchronize(b->stream));
+    if (plane == RGBDSEG_FLAGS_PLANE) {
+        CU(cudaMemcpy(dst, b->flags, b->npx, cudaMemcpyDefault));
+        return RGBDSEG_OK;
+    }
+    if (plane < 0 || plane >= rgbdseg_bank_planes(b))
+        return fail(RGBDSEG_EINVAL, "bank plane id out of range");
+    CU(cudaMemcpy(dst, b->state + (size_t)plane * b->pitch, b->npx * sizeof(float),
+                  cudaMemcpyDefault));
+    return RGBDSEG_OK;
+}
+
+int rgbdseg_bank_upload(rgbdseg_bank* b, int plane, const void* src) {
+    GUARD(b->device);
+    CU(cudaStreamSynchronize(b->stream));
+    if (plane == RGBDSEG_FLAGS_PLANE) {
+        CU(cudaMemcpy(b->flags, src, b->npx, cudaMemcpyDefault));
+        return RGBDSEG_OK;
+    }
+    if (plane < 0 || plane >= rgbdseg_bank_planes(b))
+        return fail(RGBDSEG_EINVAL, "bank plane id out of range");
+    CU(cudaMemcpy(b->state + (size_t)plane * b->pitch, src, b->npx * sizeof(float),
+                  cudaMemcpyDefault));
+    return RGBDSEG_OK;
+}
+
+// run_bank's checks (segmenter.cpp:73-75) + mode checks (:109,:123).
+static int bank_call_checks(const rgbdseg_bank* b, const rgbdseg_mixture_cfg* cfg, int mode,
+                            const char* who) {
+    if (!b) return fail(RGBDSEG_EINVAL, std::string(who) + ": null bank");
+    if (b->mode != mode)
+        return fail(RGBDSEG_EINVAL, std::string(who) + (mode == RGBDSEG_COLOR3
+                                                            ? ": bank mode is not Color3"
+                                                            : ": bank mode is not Depth1"));
+    if (int rc = validate_cfg(cfg)) return rc;
+    if (cfg->components != b->M)
+        return fail(RGBDSEG_EINVAL, "segment: config component count does not match bank");
+    return RGBDSEG_OK;
+}
+
+static int finish_mask(uint8_t* dev_mask, uint8_t* mask_out, size_t n, cudaStream_t s) {
+    if (mask_out && dev_mask != mask_out)
+        CU(cudaMemcpyAsync(mask_out, dev_mask, n, cudaMemcpyDefault, s));
+    CU(cudaStreamSynchronize(s));
+    return RGBDSEG_OK;
+}
+
+int rgbdseg_segment_color(rgbdseg_bank* b, const uint8_t* r, const uint8_t* g, const uint8_t* bl,
+                          const rgbdseg_mixture_cfg* cfg, uint8_t* mask_out) {
+    if (int rc = bank_call_checks(b, cfg, RGBDSEG_COLOR3, "segment_color")) return rc;
+    GUARD(b->device);
+    const void *dr, *dg, *db;
+    if (int rc = stage_in(r, b->npx, b->s_r, &dr, b->stream)) return rc;
+    if (int rc = stage_in(g, b->npx, b->s_g, &dg, b->stream)) return rc;
+    if (int rc = stage_in(bl, b->npx, b->s_b, &db, b->stream)) return rc;
+    uint8_t* dm = nullptr;
+    if (mask_out) {
+        if (on_device(mask_out)) {
+            dm = mask_out;
+        } else {
+            void* p;
+            if (int rc = b->s_mask.get(b->npx, &p)) return rc;
+            dm = static_cast<uint8_t*>(p);
+        }
+    }
+    CU(launch_bank_color(b->view(), to_k(*cfg), (const uint8_t*)dr, (const uint8_t*)dg,
+                         (const uint8_t*)db, dm, b->npx, b->stream));
+    return finish_mask(dm, mask_out, b->npx, b->stream);
+}
+
+int rgbdseg_segment_depth(rgbdseg_bank* b, const uint16_t* depth_mm,
+                          const rgbdseg_mixture_cfg* cfg, uint8_t* mask_out) {
+    if (int rc = bank_call_checks(b, cfg, RGBDSEG_DEPTH1, "segment_depth")) return rc;
+    GUARD(b->device);
+    const void* dd;
+    if (int rc = stage_in(depth_mm, b->npx * 2, b->s_r, &dd, b->stream)) return rc;
+    uint8_t* dm = nullptr;
+    if (mask_out) {
+        if (on_device(mask_out)) {
+            dm = mask_out;
+        } else {
+            void* p;
+            if (int rc = b->s_mask.get(b->npx, &p)) return rc;
+            dm = static_cast<uint8_t*>(p);
+        }
+    }
+    CU(launch_bank_depth(b->view(), to_k(*cfg), (const uint16_t*)dd, dm, b->npx, b->stream));
+    return finish_mask(dm, mask_out, b->npx, b->stream);
+}
+
+// ------------------------------------------------------------ fusion
+int rgbdseg_fusion_create(int width, int height, int streams, int initial_label,
+                          int counter_limit, int device, rgbdseg_fusion** out) {
+    *out = nullptr;
+    if (int rc = check_dims(width, height, streams)) return rc;
+    // reset_state, fusion.cpp:7-15
+    if (counter_limit < 1)
+        return fail(RGBDSEG_EINVAL, "reset_state: counter_limit must be >= 1");
+    if (initial_label < 0 || initial_label > 1)
+        return fail(RGBDSEG_EINVAL, "reset_state: label must be 0 or 1");
+    GUARD(device);
+    auto* f = new rgbdseg_fusion();
+    f->npx = (size_t)width * height * streams;
+    f->limit = counter_limit;
+    f->device = device;
+    int rc = dalloc(&f->out, pitch_for(f->npx));
+    if (!rc) rc = dalloc(&f->cpt, pitch_for(f->npx));
+    if (!rc) {
+        cudaError_t e = cudaStreamCreateWithFlags(&f->stream, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaMemsetAsync(f->out, initial_label, f->npx, f->stream);
+        if (e == cudaSuccess) e = cudaMemsetAsync(f->cpt, 0, f->npx, f->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(f->stream);
+        if (e != cudaSuccess) rc = cuda_fail(e, "fusion_create");
+    }
+    if (rc) {
+        rgbdseg_fusion_destroy(f);
+        return rc;
+    }
+    *out = f;
+    return RGBDSEG_OK;
+}
+
+void rgbdseg_fusion_destroy(rgbdseg_fusion* f) {
+    if (!f) return;
+    DeviceGuard g(f->device);
+    if (f->stream) cudaStreamSynchronize(f->stream);
+    dfree(f->out);
+    dfree(f->cpt);
+    if (f->stream) cudaStreamDestroy(f->stream);
+    delete f;
+}
+
+int rgbdseg_fusion_step(rgbdseg_fusion* f, const uint8_t* rgb_mask, const uint8_t* depth_mask,
+                        uint8_t* out_copy) {
+    GUARD(f->device);
+    const void *dr, *dd;
+    if (int rc = stage_in(rgb_mask, f->npx, f->s_rgb, &dr, f->stream)) return rc;
+    if (int rc = stage_in(depth_mask, f->npx, f->s_dep, &dd, f->stream)) return rc;
+    uint8_t* oc = (out_copy && on_device(out_copy)) ? out_copy : nullptr;
+    CU(launch_fuse(f->out, f->cpt, (const uint8_t*)dr, (const uint8_t*)dd, oc, f->limit, f->npx,
+                   f->stream));
+    if (out_copy && !oc) CU(cudaMemcpyAsync(out_copy, f->out, f->npx, cudaMemcpyDefault, f->stream));
+    CU(cudaStreamSynchronize(f->stream));
+    return RGBDSEG_OK;
+}
+
+int rgbdseg_fusion_download(const rgbdseg_fusion* f, uint8_t* out, int8_t* cpt) {
+    GUARD(f->device);
+    CU(cudaStreamSynchronize(f->stream));
+    if (out) CU(cudaMemcpy(out, f->out, f->npx, cudaMemcpyDefault));
+    if (cpt) CU(cudaMemcpy(cpt, f->cpt, f->npx, cudaMemcpyDefault));
+    return RGBDSEG_OK;
+}
+
+int rgbdseg_fusion_upload(rgbdseg_fusion* f, const uint8_t* out, const int8_t* cpt) {
+    GUARD(f->device);
+    CU(cudaStreamSynchronize(f->stream));
+    if (out) CU(cudaMemcpy(f->out, out, f->npx, cudaMemcpyDefault));
+    if (cpt) CU(cudaMemcpy(f->cpt, cpt, f->npx, cudaMemcpyDefault));
+    return RGBDSEG_OK;
+}
+
+// ------------------------------------------------------------ processor
+void rgbdseg_processor_defaults(rgbdseg_processor_cfg* c, int width, int height) {
+    std::memset(c, 0, sizeof *c);
+    c->width = width;
+    c->height = height;
+    c->streams = 1;
+    rgbdseg_mixture_defaults(&c->color);
+    rgbdseg_mixture_defaults(&c->depth);
+    c->depth.learning_rate = 0.01f;  // RunConfig::defaults, processor.cpp:40-41
+    c->depth.initial_sigma = 100.0f;
+    c->fusion_counter_limit = 3;
+    c->fusion_initial_label = 0;
+    c->device = 0;
+    c->host_chunks = 0;
+}
+
+void rgbdseg_processor_destroy(rgbdseg_processor* p) {
+    if (!p) return;
+    DeviceGuard g(p->cfg.device);
+    for (cudaStream_t s : {p->sc, p->sh2d, p->sd2h})
+        if (s) cudaStreamSynchronize(s);
+    for (auto& sl : p->slot) {
+        dfree(sl.r);
+        dfree(sl.g);
+        dfree(sl.b);
+        dfree(sl.d);
+        dfree(sl.rgbm);
+        dfree(sl.depm);
+        for (cudaEvent_t ev : {sl.h2d_done, sl.k_done, sl.d2h_done})
+            if (ev) cudaEventDestroy(ev);
+    }
+    for (cudaEvent_t ev : p->chunk_d2h)
+        if (ev) cudaEventDestroy(ev);
+    for (cudaStream_t s : {p->sc, p->sh2d, p->sd2h})
+        if (s) cudaStreamDestroy(s);
+    rgbdseg_bank_destroy(p->color);
+    rgbdseg_bank_destroy(p->depth);
+    rgbdseg_fusion_destroy(p->fusion);
+    delete p;
+}
+
+int rgbdseg_processor_create(const rgbdseg_processor_cfg* cfg, rgbdseg_processor** out) {
+    *out = nullptr;
+    if (int rc = check_dims(cfg->width, cfg->height, cfg->streams)) return rc;
+    // RunConfig::validate, processor.cpp:45-58 (the parts on this path)
+    if (int rc = validate_cfg(&cfg->color)) return rc;
+    if (int rc = validate_cfg(&cfg->depth)) return rc;
+    if (cfg->fusion_counter_limit < 1)
+        return fail(RGBDSEG_EINVAL, "config: fusion counter_limit must be >= 1");
+    if (cfg->fusion_initial_label < 0 || cfg->fusion_initial_label > 1)
+        return fail(RGBDSEG_EINVAL, "config: fusion initial_label must be 0 or 1");
+    GUARD(cfg->device);
+    auto* p = new rgbdseg_processor();
+    p->cfg = *cfg;
+    p->npx = (size_t)cfg->width * cfg->height * cfg->streams;
+    int rc = rgbdseg_bank_create(cfg->width, cfg->height, cfg->streams, RGBDSEG_COLOR3,
+                                 &cfg->color, cfg->device, &p->color);
+    if (!rc)
+        rc = rgbdseg_bank_create(cfg->width, cfg->height, cfg->streams, RGBDSEG_DEPTH1,
+                                 &cfg->depth, cfg->device, &p->depth);
+    if (!rc)
+        rc = rgbdseg_fusion_create(cfg->width, cfg->height, cfg->streams,
+                                   cfg->fusion_initial_label, cfg->fusion_counter_limit,
+                                   cfg->device, &p->fusion);
+    if (!rc) {
+        // Host frames stream through two device slots in chunks so the H2D of
+        // chunk k+1, the kernel of chunk k and the D2H of chunk k-1 overlap.
+        int chunks = cfg->host_chunks;
+        if (chunks <= 0) chunks = (int)std::min<size_t>(8, std::max<size_t>(1, p->npx >> 21));
+        p->nchunks = chunks;
+        p->chunk = pitch_for((p->npx + chunks - 1) / chunks);
+        cudaError_t e = cudaSuccess;
+        for (cudaStream_t* s : {&p->sc, &p->sh2d, &p->sd2h})
+            if (e == cudaSuccess) e = cudaStreamCreateWithFlags(s, cudaStreamNonBlocking);
+        for (auto& sl : p->slot)
+            for (cudaEvent_t* ev : {&sl.h2d_done, &sl.k_done, &sl.d2h_done})
+                if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+        p->chunk_d2h.assign(chunks, nullptr);
+        for (auto& ev : p->chunk_d2h)
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+        if (e != cudaSuccess) rc = cuda_fail(e, "processor_create");
+    }
+    if (rc) {
+        rgbdseg_processor_destroy(p);
+        return rc;
+    }
+    *out = p;
+    return RGBDSEG_OK;
+}
+
+static int ensure_slots(rgbdseg_processor* p) {
+    for (auto& sl : p->slot) {
+        if (sl.r) continue;
+        int rc = dalloc(&sl.r, p->chunk);
+        if (!rc) rc = dalloc(&sl.g, p->chunk);
+        if (!rc) rc = dalloc(&sl.b, p->chunk);
+        if (!rc) rc = dalloc(&sl.d, p->chunk);
+        if (!rc) rc = dalloc(&sl.rgbm, p->chunk);
+        if (!rc) rc = dalloc(&sl.depm, p->chunk);
+        if (rc) return rc;
+    }
+    return RGBDSEG_OK;
+}
+
+static FusedArgs base_args(const rgbdseg_processor* p) {
+    FusedArgs a{};
+    a.color = p->color->view();
+    a.depth = p->depth->view();
+    a.ck = to_k(p->cfg.color);
+    a.dk = to_k(p->cfg.depth);
+    a.limit = p->cfg.fusion_counter_limit;
+    return a;
+}
+
+int rgbdseg_processor_submit(rgbdseg_processor* p, const uint8_t* r, const uint8_t* g,
+                             const uint8_t* b, const uint16_t* depth, uint8_t* fused_out,
+                             uint8_t* rgb_out, uint8_t* depth_out) {
+    if (!r || !g || !b || !depth) return fail(RGBDSEG_EINVAL, "process: null input plane");
+    GUARD(p->cfg.device);
+    const bool dr = on_device(r), dg = on_device(g), db = on_device(b), dd = on_device(depth);
+    const bool dfo = on_device(fused_out), dro = on_device(rgb_out), ddo = on_device(depth_out);
+    const bool all_device = dr && dg && db && dd && (!fused_out || dfo) && (!rgb_out || dro) &&
+                            (!depth_out || ddo);
+    FusedArgs a = base_args(p);
+    a.out = p->fusion->out;
+    a.cpt = p->fusion->cpt;
+    if (all_device) {  // device-resident frames: one launch over every pixel
+        a.r = r;
+        a.g = g;
+        a.b = b;
+        a.d = depth;
+        a.rgb_mask = rgb_out;
+        a.depth_mask = depth_out;
+        a.fused_copy = fused_out;
+        a.base = 0;
+        a.n = p->npx;
+        for (cudaEvent_t ev : p->chunk_d2h)  // a host-frame emit may still read out
+            CU(cudaStreamWaitEvent(p->sc, ev, 0));
+        CU(launch_fused(a, p->variant, p->sc));
+        ++p->frames;
+        return RGBDSEG_OK;
+    }
+    if (int rc = ensure_slots(p)) return rc;
+    for (int c = 0; c < p->nchunks; ++c) {
+        const size_t lo = (size_t)c * p->chunk;
+        if (lo >= p->npx) break;
+        const size_t n = std::min(p->chunk, p->npx - lo);
+        Slot& sl = p->slot[p->seq++ & 1];
+        // ingest: wait until the previous kernel on this slot consumed it
+        CU(cudaStreamWaitEvent(p->sh2d, sl.k_done, 0));
+        a.r = dr ? r + lo : sl.r;
+        a.g = dg ? g + lo : sl.g;
+        a.b = db ? b + lo : sl.b;
+        a.d = dd ? depth + lo : sl.d;
+        if (!dr) CU(cudaMemcpyAsync(sl.r, r + lo, n, cudaMemcpyDefault, p->sh2d));
+        if (!dg) CU(cudaMemcpyAsync(sl.g, g + lo, n, cudaMemcpyDefault, p->sh2d));
+        if (!db) CU(cudaMemcpyAsync(sl.b, b + lo, n, cudaMemcpyDefault, p->sh2d));
+        if (!dd) CU(cudaMemcpyAsync(sl.d, depth + lo, n * 2, cudaMemcpyDefault, p->sh2d));
+        CU(cudaEventRecord(sl.h2d_done, p->sh2d));
+        // process: inputs landed, previous emit of this slot's masks and of
+        // this chunk's fused labels finished
+        CU(cudaStreamWaitEvent(p->sc, sl.h2d_done, 0));
+        CU(cudaStreamWaitEvent(p->sc, sl.d2h_done, 0));
+        CU(cudaStreamWaitEvent(p->sc, p->chunk_d2h[c], 0));
+        a.rgb_mask = rgb_out ? (dro ? rgb_out + lo : sl.rgbm) : nullptr;
+        a.depth_mask = depth_out ? (ddo ? depth_out + lo : sl.depm) : nullptr;
+        a.fused_copy = (fused_out && dfo) ? fused_out + lo : nullptr;
+        a.base = lo;
+        a.n = n;
+        a.out = p->fusion->out + lo;
+        a.cpt = p->fusion->cpt + lo;
+        CU(launch_fused(a, p->variant, p->sc));
+        CU(cudaEventRecord(sl.k_done, p->sc));
+        // emit
+        CU(cudaStreamWaitEvent(p->sd2h, sl.k_done, 0));
+        if (fused_out && !dfo)
+            CU(cudaMemcpyAsync(fused_out + lo, p->fusion->out + lo, n, cudaMemcpyDefault, p->sd2h));
+        if (rgb_out && !dro)
+            CU(cudaMemcpyAsync(rgb_out + lo, sl.rgbm, n, cudaMemcpyDefault, p->sd2h));
+        if (depth_out && !ddo)
+            CU(cudaMemcpyAsync(depth_out + lo, sl.depm, n, cudaMemcpyDefault, p->sd2h));
+        CU(cudaEventRecord(sl.d2h_done, p->sd2h));
+        CU(cudaEventRecord(p->chunk_d2h[c], p->sd2h));
+    }
+    ++p->frames;
+    return RGBDSEG_OK;
+}
+
+int rgbdseg_processor_sync(rgbdseg_processor* p) {
+    GUARD(p->cfg.device);
+    CU(cudaStreamSynchronize(p->sh2d));
+    CU(cudaStreamSynchronize(p->sc));
+    CU(cudaStreamSynchronize(p->sd2h));
+    return RGBDSEG_OK;
+}
+
+int rgbdseg_processor_process(rgbdseg_processor* p, const uint8_t* r, const uint8_t* g,
+                              const uint8_t* b, const uint16_t* depth, uint8_t* fused_out,
+                              uint8_t* rgb_out, uint8_t* depth_out) {
+    if (int rc = rgbdseg_processor_submit(p, r, g, b, depth, fused_out, rgb_out, depth_out))
+        return rc;
+    return rgbdseg_processor_sync(p);
+}
+
+int64_t rgbdseg_processor_frames(const rgbdseg_processor* p) { return p->frames; }
+rgbdseg_bank* rgbdseg_processor_color_bank(rgbdseg_processor* p) { return p->color; }
+rgbdseg_bank* rgbdseg_processor_depth_bank(rgbdseg_processor* p) { return p->depth; }
+rgbdseg_fusion* rgbdseg_processor_fusion(rgbdseg_processor* p) { return p->fusion; }
+void* rgbdseg_processor_stream(rgbdseg_processor* p) { return (void*)p->sc; }
+
+int rgbdseg_processor_set_variant(rgbdseg_processor* p, int variant) {
+    if (variant < kAuto || variant > kBulk) return fail(RGBDSEG_EINVAL, "unknown kernel variant");
+    p->variant = variant;
+    return RGBDSEG_OK;
+}
+
+// ------------------------------------------------------------ synthetic scenes
+// builtin_scenario (synthetic.cpp:234-273) resolved for one frame: the
+// illumination gain product, the object's lround'ed waypoint position and
+// the active shadow / flicker events (render_frame, synthetic.cpp:124-134).
+int rgbdseg_render_scenario(char name, int width, int height, int streams, uint64_t seed0,
+                            int frame, uint8_t* r, uint8_t* g, uint8_t* b, uint16_t* depth,
+                            uint8_t* gt, int device, void* stream) {
+    if (name != 'A' && name != 'B')
+        return fail(RGBDSEG_EINVAL, std::string("unknown scenario '") + name + "' (known: A, B)");
+    if (int rc = check_dims(width, height, streams)) return rc;
+    GUARD(device);
+    SceneFrame sc{};
+    sc.width = width;
+    sc.height = height;
+    sc.streams = streams;
+    sc.seed0 = seed0;
+    sc.frame = frame;
+    sc.base_depth_mm = 2000;
+    sc.depth_texture_mm = 30;
+    sc.color_texture = 8;
+    // the 24x24 box, (40,100) at frame 0 -> (600,320) at frame 299
+    struct Wp {
+        int f;
+        double x, y;
+    } wp[2] = {{0, 40, 100}, {299, 600, 320}};
+    double x = wp[0].x, y = wp[0].y;
+    if (frame >= wp[1].f) {
+        x = wp[1].x;
+        y = wp[1].y;
+    } else if (frame > wp[0].f) {
+        const double t = (double)(frame - wp[0].f) / (double)(wp[1].f - wp[0].f);
+        x = wp[0].x + t * (wp[1].x - wp[0].x);
+        y = wp[0].y + t * (wp[1].y - wp[0].y);
+    }
+    sc.n_obj = 1;
+    sc.orect[0][0] = (int)std::lround(x);
+    sc.orect[0][1] = (int)std::lround(y);
+    sc.orect[0][2] = 24;
+    sc.orect[0][3] = 24;
+    sc.ocolor[0][0] = 230;
+    sc.ocolor[0][1] = 40;
+    sc.ocolor[0][2] = 220;
+    sc.odepth[0] = 400;
+    sc.gain = 1.0;
+    if (name == 'A') {
+        const struct {
+            int s, e;
+            double g;
+        } il[2] = {{100, 112, 1.5}, {200, 212, 0.6}};
+        for (auto& e : il)
+            if (frame >= e.s && frame < e.e) sc.gain *= e.g;
+        if (frame >= 150 && frame < 180) {
+            sc.n_shadow = 1;
+            const int rc[4] = {300, 300, 200, 120};
+            std::memcpy(sc.srect[0], rc, sizeof rc);
+            sc.sdarken[0] = 0.6;
+        }
+        if (frame >= 0 && frame < 300) {
+            sc.n_flicker = 1;
+            const int rc[4] = {40, 40, 80, 60};
+            std::memcpy(sc.frect[0], rc, sizeof rc);
+            sc.fcs[0] = 3.0;
+            sc.fds[0] = 30.0;
+        }
+        sc.ncs = 1.0;
+        sc.nds = 1.0;
+    } else {
+        const double gains[10] = {1.4, 0.7, 1.25, 0.8, 1.35, 0.75, 1.2, 0.85, 1.3, 0.9};
+        for (int i = 0; i < 10; ++i)
+            if (frame >= 30 + 25 * i && frame < 30 + 25 * (i + 1)) sc.gain *= gains[i];
+        if (frame >= 0 && frame < 300) {
+            sc.n_flicker = 1;
+            const int rc[4] = {400, 60, 160, 120};
+            std::memcpy(sc.frect[0], rc, sizeof rc);
+            sc.fcs[0] = 12.0;
+            sc.fds[0] = 40.0;
+        }
+        sc.ncs = 1.5;
+        sc.nds = 2.0;
+    }
+    CU(launch_render(sc, r, g, b, depth, gt, (cudaStream_t)stream));
+    if (!stream) CU(cudaStreamSynchronize(0));
+    return RGBDSEG_OK;
+}
+
+}  // extern "C"

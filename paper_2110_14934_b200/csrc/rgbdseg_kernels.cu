@@ -1,0 +1,491 @@
+// rgbdseg_kernels.cu -- sm_100a kernels for the RGB-D GMM hot path.
+//
+// K1  k_fused_*      colour GMM + depth GMM + List-1 fusion in ONE pass per
+//                    pixel (SequenceProcessor::process, processor.cpp:158-184
+//                    -> segment_color/segment_depth segmenter.cpp:107-131 ->
+//                    run_bank :70-99 -> step_pixel mixture.cpp:148-154 ->
+//                    fuse_step fusion.cpp:17-46).  Masks stay in registers.
+// K1b k_bank_*       one bank alone (segment_color / segment_depth drop-ins).
+// K1c k_fuse         fuse_step alone.
+// K0  k_mix_*        the per-pixel API (init_mixture / step_pixel) batched.
+// K3  k_render       synthetic scene generator (synthetic.cpp:119-195).
+//
+// All kernels are memory-bound elementwise work: one thread per pixel, the
+// mixture in registers for the whole update, structure-of-arrays planes in
+// HBM so every plane access of a warp is one fully coalesced 128-byte line.
+// Built with -fmad=false -prec-div=true -prec-sqrt=true -ftz=false and the
+// arithmetic spelled with explicit _rn intrinsics (gmm_pixel.cuh).
+#include <atomic>
+#include <cstdio>
+
+#include "rgbdseg_kernels.cuh"
+
+namespace rgbdseg_b200 {
+
+namespace {
+std::atomic<uint64_t> g_launches{0};
+
+constexpr int kThreads = 256;
+
+inline unsigned blocks_for(size_t n) {
+    return static_cast<unsigned>((n + kThreads - 1) / kThreads);
+}
+
+// Streaming loads/stores: every state word is touched once per frame.
+template <typename T>
+__device__ __forceinline__ T ld_stream(const T* p) {
+    return __ldcs(p);
+}
+template <typename T>
+__device__ __forceinline__ void st_stream(T* p, T v) {
+    __stcs(p, v);
+}
+
+template <int M, int C>
+__device__ __forceinline__ void load_mix(const BankView& bk, size_t j, Mixture<M, C>& m) {
+    const float* s = bk.state + j;
+    const size_t P = bk.pitch;
+#pragma unroll
+    for (int i = 0; i < M; ++i)
+#pragma unroll
+        for (int c = 0; c < C; ++c) m.mu[i][c] = ld_stream(s + (size_t)(i * C + c) * P);
+#pragma unroll
+    for (int i = 0; i < M; ++i) m.var[i] = ld_stream(s + (size_t)(M * C + i) * P);
+#pragma unroll
+    for (int i = 0; i < M; ++i) m.w[i] = ld_stream(s + (size_t)(M * C + M + i) * P);
+}
+
+// Dense store of every plane (ModelBank::scatter, segmenter.cpp:49-56).
+template <int M, int C>
+__device__ __forceinline__ void store_mix(const BankView& bk, size_t j, const Mixture<M, C>& m) {
+    float* s = bk.state + j;
+    const size_t P = bk.pitch;
+#pragma unroll
+    for (int i = 0; i < M; ++i)
+#pragma unroll
+        for (int c = 0; c < C; ++c) st_stream(s + (size_t)(i * C + c) * P, m.mu[i][c]);
+#pragma unroll
+    for (int i = 0; i < M; ++i) st_stream(s + (size_t)(M * C + i) * P, m.var[i]);
+#pragma unroll
+    for (int i = 0; i < M; ++i) st_stream(s + (size_t)(M * C + M + i) * P, m.w[i]);
+}
+
+// Elided store: identical memory image to store_mix, but words whose bits
+// did not change are not rewritten.  Only the matched / replaced component's
+// mean and variance can change in a step (mixture.cpp:105-113, 125-128); the
+// weights are compared individually.  touched < 0 means "all" (init).
+template <int M, int C>
+__device__ __forceinline__ void store_mix_elide(const BankView& bk, size_t j,
+                                                const Mixture<M, C>& m, int touched,
+                                                const float (&w_old)[M]) {
+    float* s = bk.state + j;
+    const size_t P = bk.pitch;
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        if (touched < 0 || touched == i) {
+#pragma unroll
+            for (int c = 0; c < C; ++c) st_stream(s + (size_t)(i * C + c) * P, m.mu[i][c]);
+            st_stream(s + (size_t)(M * C + i) * P, m.var[i]);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < M; ++i)
+        if (touched < 0 || __float_as_uint(m.w[i]) != __float_as_uint(w_old[i]))
+            st_stream(s + (size_t)(M * C + M + i) * P, m.w[i]);
+}
+
+// run_bank's per-pixel body (segmenter.cpp:80-96) on a loaded mixture.
+// Returns the label; `touched` reports what changed for the elided store.
+template <int M, int C>
+__device__ __forceinline__ uint32_t bank_pixel(Mixture<M, C>& m, const float (&v)[C],
+                                               bool initialised, const MixCfg& k,
+                                               int& touched) {
+    if (!initialised) {
+        gmm_init(m, v, k);
+        touched = -1;
+        return 0u;
+    }
+    return gmm_step(m, v, k, touched);
+}
+
+// ---------------------------------------------------------------- K1 fused
+template <int MC, int MD, bool kElide>
+__global__ void __launch_bounds__(kThreads) k_fused_ldg(const __grid_constant__ FusedArgs a) {
+    const size_t i = (size_t)blockIdx.x * kThreads + threadIdx.x;
+    if (i >= a.n) return;
+    const size_t j = a.base + i;
+
+    // Issue every load of the pixel before any math: inputs, flags, fusion
+    // state and both mixtures (40 planes at M=5) are independent requests.
+    const float vc[3] = {(float)ld_stream(a.r + i), (float)ld_stream(a.g + i),
+                         (float)ld_stream(a.b + i)};
+    const uint32_t raw = ld_stream(a.d + i);
+    const bool cinit = ld_stream(a.color.flags + j) != 0;
+    const bool dinit = ld_stream(a.depth.flags + j) != 0;
+    const uint32_t out0 = ld_stream(a.out + i);
+    const int cpt0 = (int)ld_stream(a.cpt + i);
+    Mixture<MC, 3> cm;
+    Mixture<MD, 1> dm;
+    load_mix(a.color, j, cm);
+    load_mix(a.depth, j, dm);
+
+    // ---- colour stream (segment_color) ----
+    float cw_old[MC];
+#pragma unroll
+    for (int q = 0; q < MC; ++q) cw_old[q] = cm.w[q];
+    int ct = 0;
+    const uint32_t lc = bank_pixel(cm, vc, cinit, a.ck, ct);
+    if (kElide)
+        store_mix_elide(a.color, j, cm, ct, cw_old);
+    else
+        store_mix(a.color, j, cm);
+    if (!cinit) st_stream(a.color.flags + j, (uint8_t)1);
+
+    // ---- depth stream (segment_depth): raw 0 = no return ----
+    uint32_t ld = 0;
+    if (raw != 0) {
+        const float vd[1] = {(float)raw};
+        float dw_old[MD];
+#pragma unroll
+        for (int q = 0; q < MD; ++q) dw_old[q] = dm.w[q];
+        int dt = 0;
+        ld = bank_pixel(dm, vd, dinit, a.dk, dt);
+        if (kElide)
+            store_mix_elide(a.depth, j, dm, dt, dw_old);
+        else
+            store_mix(a.depth, j, dm);
+        if (!dinit) st_stream(a.depth.flags + j, (uint8_t)1);
+    }
+
+    // ---- List-1 fusion on the registered depth mask ----
+    uint32_t out = out0;
+    int cpt = cpt0;
+    fuse_pixel(lc, ld, a.limit, out, cpt);
+    if (!kElide || out != out0) st_stream(a.out + i, (uint8_t)out);
+    if (!kElide || cpt != cpt0) st_stream(a.cpt + i, (int8_t)cpt);
+    if (a.rgb_mask) st_stream(a.rgb_mask + i, (uint8_t)lc);
+    if (a.depth_mask) st_stream(a.depth_mask + i, (uint8_t)ld);
+    if (a.fused_copy) st_stream(a.fused_copy + i, (uint8_t)out);
+}
+
+// ---------------------------------------------------------------- K1b banks
+template <int M>
+__global__ void __launch_bounds__(kThreads)
+    k_bank_color(BankView bk, MixCfg k, const uint8_t* __restrict__ r,
+                 const uint8_t* __restrict__ g, const uint8_t* __restrict__ b,
+                 uint8_t* __restrict__ mask, size_t n) {
+    const size_t j = (size_t)blockIdx.x * kThreads + threadIdx.x;
+    if (j >= n) return;
+    const float v[3] = {(float)r[j], (float)g[j], (float)b[j]};
+    const bool init = bk.flags[j] != 0;
+    Mixture<M, 3> m;
+    load_mix(bk, j, m);
+    int t;
+    const uint32_t lab = bank_pixel(m, v, init, k, t);
+    store_mix(bk, j, m);
+    if (!init) bk.flags[j] = 1;
+    if (mask) mask[j] = (uint8_t)lab;
+}
+
+template <int M>
+__global__ void __launch_bounds__(kThreads)
+    k_bank_depth(BankView bk, MixCfg k, const uint16_t* __restrict__ d,
+                 uint8_t* __restrict__ mask, size_t n) {
+    const size_t j = (size_t)blockIdx.x * kThreads + threadIdx.x;
+    if (j >= n) return;
+    const uint32_t raw = d[j];
+    uint32_t lab = 0;
+    if (raw != 0) {  // segmenter.cpp:84,128
+        const float v[1] = {(float)raw};
+        const bool init = bk.flags[j] != 0;
+        Mixture<M, 1> m;
+        load_mix(bk, j, m);
+        int t;
+        lab = bank_pixel(m, v, init, k, t);
+        store_mix(bk, j, m);
+        if (!init) bk.flags[j] = 1;
+    }
+    if (mask) mask[j] = (uint8_t)lab;
+}
+
+// ModelBank ctor state (segmenter.cpp:24-34): means 0, var sigma0^2, w (1,0,..)
+__global__ void k_bank_reset(BankView bk, float sigma0, size_t n) {
+    const size_t j = (size_t)blockIdx.x * kThreads + threadIdx.x;
+    if (j >= n) return;
+    const float var0 = fmul(sigma0, sigma0);
+    const int M = bk.M, C = bk.C;
+    for (int p = 0; p < M * C; ++p) bk.state[(size_t)p * bk.pitch + j] = 0.0f;
+    for (int q = 0; q < M; ++q) {
+        bk.state[(size_t)(M * C + q) * bk.pitch + j] = var0;
+        bk.state[(size_t)(M * C + M + q) * bk.pitch + j] = q == 0 ? 1.0f : 0.0f;
+    }
+    bk.flags[j] = 0;
+}
+
+// ---------------------------------------------------------------- K1c fusion
+__global__ void __launch_bounds__(kThreads)
+    k_fuse(uint8_t* __restrict__ out, int8_t* __restrict__ cpt, const uint8_t* __restrict__ rgb,
+           const uint8_t* __restrict__ dep, uint8_t* __restrict__ out_copy, int limit, size_t n) {
+    const size_t j = (size_t)blockIdx.x * kThreads + threadIdx.x;
+    if (j >= n) return;
+    uint32_t o = out[j];
+    int c = cpt[j];
+    fuse_pixel(rgb[j], dep[j], limit, o, c);
+    out[j] = (uint8_t)o;
+    cpt[j] = (int8_t)c;
+    if (out_copy) out_copy[j] = (uint8_t)o;
+}
+
+// ---------------------------------------------------------------- K0 per pixel
+template <int M, int C>
+__device__ void rec_step(PixRec& rec, const float* vals, const MixCfg& k, uint8_t& lab) {
+    Mixture<M, C> m;
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+#pragma unroll
+        for (int c = 0; c < C; ++c) m.mu[i][c] = rec.means[i * C + c];
+        m.var[i] = rec.variances[i];
+        m.w[i] = rec.weights[i];
+    }
+    float v[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) v[c] = vals[c];
+    lab = (uint8_t)gmm_step(m, v, k);
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+#pragma unroll
+        for (int c = 0; c < C; ++c) rec.means[i * C + c] = m.mu[i][c];
+        rec.variances[i] = m.var[i];
+        rec.weights[i] = m.w[i];
+    }
+}
+
+template <int M>
+__device__ void rec_step_c(PixRec& rec, const float* vals, const MixCfg& k, uint8_t& lab) {
+    switch (rec.channels) {
+        case 1: rec_step<M, 1>(rec, vals, k, lab); break;
+        case 2: rec_step<M, 2>(rec, vals, k, lab); break;
+        case 3: rec_step<M, 3>(rec, vals, k, lab); break;
+        case 4: rec_step<M, 4>(rec, vals, k, lab); break;
+        default: lab = 255; break;
+    }
+}
+
+__global__ void k_mix_step(PixRec* recs, const float* values, int channels, size_t n, MixCfg k,
+                           uint8_t* labels) {
+    const size_t j = (size_t)blockIdx.x * kThreads + threadIdx.x;
+    if (j >= n) return;
+    PixRec rec = recs[j];
+    uint8_t lab = 255;
+    if (rec.channels == channels) {
+        const float* v = values + j * channels;
+        switch (rec.components) {  // step_pixel loops over mixture.components
+            case 3: rec_step_c<3>(rec, v, k, lab); break;
+            case 4: rec_step_c<4>(rec, v, k, lab); break;
+            case 5: rec_step_c<5>(rec, v, k, lab); break;
+            default: break;
+        }
+    }
+    if (lab != 255) recs[j] = rec;
+    labels[j] = lab;
+}
+
+__global__ void k_mix_init(const float* values, int channels, size_t n, MixCfg k, int M,
+                           PixRec* out) {
+    const size_t j = (size_t)blockIdx.x * kThreads + threadIdx.x;
+    if (j >= n) return;
+    PixRec rec;
+    rec.components = M;
+    rec.channels = channels;
+    for (int q = 0; q < 20; ++q) rec.means[q] = 0.0f;
+    const float var0 = fmul(k.sigma0, k.sigma0);
+    for (int q = 0; q < 5; ++q) {
+        rec.variances[q] = q < M ? var0 : 0.0f;
+        rec.weights[q] = q == 0 ? 1.0f : 0.0f;
+    }
+    for (int c = 0; c < channels; ++c) rec.means[c] = values[j * channels + c];
+    out[j] = rec;
+}
+
+// ---------------------------------------------------------------- K3 render
+__device__ __forceinline__ uint64_t splitmix(uint64_t z) {
+    z += 0x9e3779b97f4a7c15ULL;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ uint64_t hash5(uint64_t seed, uint64_t st, uint64_t fr, uint64_t px,
+                                          uint64_t ch) {  // synthetic.cpp:66-74
+    uint64_t h = splitmix(seed ^ 0x6a09e667f3bcc908ULL);
+    h = splitmix(h ^ st);
+    h = splitmix(h ^ fr);
+    h = splitmix(h ^ px);
+    return splitmix(h ^ ch);
+}
+
+__device__ __forceinline__ double gauss5(uint64_t seed, uint64_t st, uint64_t fr, uint64_t px,
+                                         uint64_t ch) {  // synthetic.cpp:76-83
+    const uint64_t h = hash5(seed, st, fr, px, ch);
+    const double u1 = __ddiv_rn(__dadd_rn((double)(h >> 32), 1.0), 4294967297.0);
+    const double u2 = __ddiv_rn((double)(h & 0xffffffffULL), 4294967296.0);
+    return __dmul_rn(__dsqrt_rn(__dmul_rn(-2.0, log(u1))),
+                     cos(__dmul_rn(__dmul_rn(2.0, 3.141592653589793), u2)));
+}
+
+__device__ __forceinline__ bool in_rect(const int (&rc)[4], int x, int y) {
+    return x >= rc[0] && x < rc[0] + rc[2] && y >= rc[1] && y < rc[1] + rc[3];
+}
+
+__global__ void k_render(const __grid_constant__ SceneFrame sc, uint8_t* R, uint8_t* G,
+                         uint8_t* B, uint16_t* D, uint8_t* GT, size_t n) {
+    const size_t idx = (size_t)blockIdx.x * kThreads + threadIdx.x;
+    if (idx >= n) return;
+    const size_t per = (size_t)sc.width * sc.height;
+    const uint64_t s = idx / per;
+    const uint64_t pix = idx - s * per;
+    const int x = (int)(pix % sc.width), y = (int)(pix / sc.width);
+    const uint64_t seed = sc.seed0 + s;
+    const int w = sc.width, h = sc.height;
+    double base[3] = {__dadd_rn(60.0, __ddiv_rn(__dmul_rn(90.0, (double)x), (double)w)),
+                      __dadd_rn(70.0, __ddiv_rn(__dmul_rn(90.0, (double)y), (double)h)),
+                      __dadd_rn(80.0, __ddiv_rn(__dmul_rn(80.0, (double)(x + y)), (double)(w + h)))};
+    const uint64_t span = (uint64_t)(2.0 * sc.color_texture + 1.0);
+    for (int c = 0; c < 3; ++c) {
+        const uint64_t t = hash5(seed, 1, 0, pix, c);
+        base[c] = __dadd_rn(base[c], __dsub_rn((double)(t % span), (double)sc.color_texture));
+    }
+    double depth = sc.base_depth_mm;
+    if (sc.depth_texture_mm > 0) {
+        const uint64_t t = hash5(seed, 2, 0, pix, 0);
+        depth = __dadd_rn(depth, __dsub_rn((double)(t % (uint64_t)(2 * sc.depth_texture_mm + 1)),
+                                           (double)sc.depth_texture_mm));
+    }
+    int top = -1;
+    for (int o = 0; o < sc.n_obj; ++o)
+        if (in_rect(sc.orect[o], x, y)) top = o;
+    uint8_t label = 0;
+    if (top >= 0) {
+        for (int c = 0; c < 3; ++c) base[c] = sc.ocolor[top][c];
+        depth = __dsub_rn(depth, (double)sc.odepth[top]);
+        label = 1;
+    }
+    double col[3] = {__dmul_rn(base[0], sc.gain), __dmul_rn(base[1], sc.gain),
+                     __dmul_rn(base[2], sc.gain)};
+    for (int e = 0; e < sc.n_shadow; ++e)
+        if (in_rect(sc.srect[e], x, y))
+            for (int c = 0; c < 3; ++c) col[c] = __dmul_rn(col[c], sc.sdarken[e]);
+    for (int e = 0; e < sc.n_flicker; ++e) {
+        if (!in_rect(sc.frect[e], x, y)) continue;
+        for (int c = 0; c < 3; ++c)
+            col[c] = __dadd_rn(col[c], __dmul_rn(sc.fcs[e], gauss5(seed, 5, sc.frame, pix, c)));
+        depth = __dadd_rn(depth, __dmul_rn(sc.fds[e], gauss5(seed, 6, sc.frame, pix, 0)));
+    }
+    for (int c = 0; c < 3; ++c)
+        col[c] = __dadd_rn(col[c], __dmul_rn(sc.ncs, gauss5(seed, 3, sc.frame, pix, c)));
+    depth = __dadd_rn(depth, __dmul_rn(sc.nds, gauss5(seed, 4, sc.frame, pix, 0)));
+    long q[3];
+    for (int c = 0; c < 3; ++c) {
+        q[c] = lround(col[c]);
+        q[c] = q[c] < 0 ? 0 : (q[c] > 255 ? 255 : q[c]);
+    }
+    long dq = lround(depth);
+    dq = dq < 1 ? 1 : (dq > 65535 ? 65535 : dq);
+    R[idx] = (uint8_t)q[0];
+    G[idx] = (uint8_t)q[1];
+    B[idx] = (uint8_t)q[2];
+    D[idx] = (uint16_t)dq;
+    if (GT) GT[idx] = label;
+}
+
+template <typename K, typename... Args>
+cudaError_t go(K kernel, size_t n, cudaStream_t s, Args... args) {
+    if (n == 0) return cudaSuccess;
+    kernel<<<blocks_for(n), kThreads, 0, s>>>(args...);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cudaGetLastError();
+}
+
+template <int MC, int MD>
+cudaError_t fused_md(const FusedArgs& a, int variant, cudaStream_t s) {
+    if (a.n == 0) return cudaSuccess;
+    if (variant == kLdgElide)
+        k_fused_ldg<MC, MD, true><<<blocks_for(a.n), kThreads, 0, s>>>(a);
+    else
+        k_fused_ldg<MC, MD, false><<<blocks_for(a.n), kThreads, 0, s>>>(a);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cudaGetLastError();
+}
+
+template <int MC>
+cudaError_t fused_mc(const FusedArgs& a, int variant, cudaStream_t s) {
+    switch (a.depth.M) {
+        case 3: return fused_md<MC, 3>(a, variant, s);
+        case 4: return fused_md<MC, 4>(a, variant, s);
+        case 5: return fused_md<MC, 5>(a, variant, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+cudaError_t launch_fused(const FusedArgs& a, int variant, cudaStream_t s) {
+    switch (a.color.M) {
+        case 3: return fused_mc<3>(a, variant, s);
+        case 4: return fused_mc<4>(a, variant, s);
+        case 5: return fused_mc<5>(a, variant, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_bank_color(BankView bk, const MixCfg& k, const uint8_t* r, const uint8_t* g,
+                              const uint8_t* b, uint8_t* mask, size_t n, cudaStream_t s) {
+    switch (bk.M) {
+        case 3: return go(k_bank_color<3>, n, s, bk, k, r, g, b, mask, n);
+        case 4: return go(k_bank_color<4>, n, s, bk, k, r, g, b, mask, n);
+        case 5: return go(k_bank_color<5>, n, s, bk, k, r, g, b, mask, n);
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_bank_depth(BankView bk, const MixCfg& k, const uint16_t* d, uint8_t* mask,
+                              size_t n, cudaStream_t s) {
+    switch (bk.M) {
+        case 3: return go(k_bank_depth<3>, n, s, bk, k, d, mask, n);
+        case 4: return go(k_bank_depth<4>, n, s, bk, k, d, mask, n);
+        case 5: return go(k_bank_depth<5>, n, s, bk, k, d, mask, n);
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_bank_reset(BankView bk, float sigma0, size_t n, cudaStream_t s) {
+    return go(k_bank_reset, n, s, bk, sigma0, n);
+}
+
+cudaError_t launch_fuse(uint8_t* out, int8_t* cpt, const uint8_t* rgb, const uint8_t* dep,
+                        uint8_t* out_copy, int limit, size_t n, cudaStream_t s) {
+    return go(k_fuse, n, s, out, cpt, rgb, dep, out_copy, limit, n);
+}
+
+cudaError_t launch_mix_init(const float* values, int channels, size_t n, const MixCfg& k, int M,
+                            PixRec* out, cudaStream_t s) {
+    return go(k_mix_init, n, s, values, channels, n, k, M, out);
+}
+
+cudaError_t launch_mix_step(PixRec* recs, const float* values, int channels, size_t n,
+                            const MixCfg& k, uint8_t* labels, cudaStream_t s) {
+    return go(k_mix_step, n, s, recs, values, channels, n, k, labels);
+}
+
+cudaError_t launch_render(const SceneFrame& sc, uint8_t* r, uint8_t* g, uint8_t* b, uint16_t* d,
+                          uint8_t* gt, cudaStream_t s) {
+    const size_t n = (size_t)sc.width * sc.height * sc.streams;
+    if (n == 0) return cudaSuccess;
+    k_render<<<blocks_for(n), kThreads, 0, s>>>(sc, r, g, b, d, gt, n);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cudaGetLastError();
+}
+
+uint64_t launches() { return g_launches.load(); }
+
+}  // namespace rgbdseg_b200

@@ -1,0 +1,96 @@
+// rgbdseg_kernels.cuh -- launch interface between the C-ABI host runtime
+// (rgbdseg_capi.cu) and the sm_100a kernels (rgbdseg_kernels.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "gmm_pixel.cuh"
+
+namespace rgbdseg_b200 {
+
+// Device layout of one bank: `planes` float planes of `pitch` elements each,
+// plane order = ModelBank (segmenter.hpp:51-54): mean(i,c) = i*C + c,
+// variance(i) = M*C + i, weight(i) = M*C + M + i.  Flags: one uint8 plane.
+struct BankView {
+    float* state;
+    uint8_t* flags;
+    size_t pitch;
+    int M;
+    int C;
+};
+
+struct FusedArgs {
+    // inputs for pixels [0, n) of this launch (pre-offset by the caller)
+    const uint8_t* r;
+    const uint8_t* g;
+    const uint8_t* b;
+    const uint16_t* d;
+    // optional mask outputs (pre-offset), may be null
+    uint8_t* rgb_mask;
+    uint8_t* depth_mask;
+    uint8_t* fused_copy;
+    // state: pixel i of this launch is pixel base + i of the banks
+    BankView color;
+    BankView depth;
+    uint8_t* out;  // fusion state (already offset by base)
+    int8_t* cpt;
+    size_t base;
+    size_t n;
+    MixCfg ck;
+    MixCfg dk;
+    int limit;
+};
+
+enum Variant { kAuto = 0, kLdgDense = 1, kLdgElide = 2, kBulk = 3 };
+
+// All launchers return cudaGetLastError() after the launch.
+cudaError_t launch_fused(const FusedArgs& a, int variant, cudaStream_t s);
+cudaError_t launch_bank_color(BankView bank, const MixCfg& k, const uint8_t* r, const uint8_t* g,
+                              const uint8_t* b, uint8_t* mask, size_t n, cudaStream_t s);
+cudaError_t launch_bank_depth(BankView bank, const MixCfg& k, const uint16_t* d, uint8_t* mask,
+                              size_t n, cudaStream_t s);
+cudaError_t launch_bank_reset(BankView bank, float sigma0, size_t n, cudaStream_t s);
+cudaError_t launch_fuse(uint8_t* out, int8_t* cpt, const uint8_t* rgb, const uint8_t* dep,
+                        uint8_t* out_copy, int limit, size_t n, cudaStream_t s);
+
+// Per-pixel API over AoS records (rgbdseg_pixel_mixture layout).
+struct PixRec {
+    int components;
+    int channels;
+    float means[20];
+    float variances[5];
+    float weights[5];
+};
+cudaError_t launch_mix_init(const float* values, int channels, size_t n, const MixCfg& k,
+                            int M, PixRec* out, cudaStream_t s);
+// labels: 0/1, or 255 for a record whose shape the kernel cannot step.
+cudaError_t launch_mix_step(PixRec* recs, const float* values, int channels, size_t n,
+                            const MixCfg& k, uint8_t* labels, cudaStream_t s);
+
+// Synthetic scene for one frame (frame-level quantities resolved on the host).
+struct SceneFrame {
+    int width, height, streams;
+    uint64_t seed0;
+    int frame;
+    int base_depth_mm, depth_texture_mm, color_texture;
+    double gain;
+    int n_obj;
+    int orect[4][4];
+    int ocolor[4][3];
+    int odepth[4];
+    int n_shadow;
+    int srect[16][4];
+    double sdarken[16];
+    int n_flicker;
+    int frect[16][4];
+    double fcs[16], fds[16];
+    double ncs, nds;
+};
+cudaError_t launch_render(const SceneFrame& sc, uint8_t* r, uint8_t* g, uint8_t* b, uint16_t* d,
+                          uint8_t* gt, cudaStream_t s);
+
+uint64_t launches();
+
+}  // namespace rgbdseg_b200

@@ -1,0 +1,576 @@
+"""Python mirror of the reference ``_rgbdseg`` binding for the hot path.
+
+Names, argument meaning and error behaviour follow the reference pybind11
+module (/root/reference/proj/python/module.cpp:40-193) and the C++ API it
+wraps (include/rgbdseg/{mixture,segmenter,fusion,processor}.hpp).  Everything
+computes on the GPU through the C-ABI (include/rgbdseg_c.h); there is no CPU
+path.  Additions beyond the reference binding -- which binds no frame-level
+API -- are the device banks (``ModelBank``, ``segment_color``,
+``segment_depth``), the fused ``SequenceProcessor`` and batched per-pixel
+records, all accepting numpy arrays (host) or CUDA tensors (device).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, lib
+
+# ------------------------------------------------------------------ buffers
+
+PIXEL_MIXTURE_DTYPE = np.dtype(
+    [("components", "<i4"), ("channels", "<i4"), ("means", "<f4", 20),
+     ("variances", "<f4", 5), ("weights", "<f4", 5)], align=True)
+assert PIXEL_MIXTURE_DTYPE.itemsize == C.sizeof(_lib.PixelMixtureRec)
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+def _buf(x, dtype, n: int, what: str, writable=False):
+    """Raw pointer of a host numpy array or a CUDA tensor holding n elements."""
+    if x is None:
+        return None
+    if _is_torch(x):
+        import torch
+
+        want = {np.uint8: torch.uint8, np.uint16: torch.uint16, np.int8: torch.int8,
+                np.float32: torch.float32}[dtype]
+        if x.dtype != want:
+            raise ValueError(f"{what}: expected dtype {want}, got {x.dtype}")
+        if not x.is_contiguous() or x.numel() != n:
+            raise ValueError(f"{what}: expected a contiguous tensor of {n} elements")
+        return x.data_ptr()
+    if not isinstance(x, np.ndarray) or x.dtype != dtype or not x.flags.c_contiguous:
+        raise ValueError(f"{what}: expected a C-contiguous numpy array of dtype {np.dtype(dtype)}")
+    if x.size != n:
+        raise ValueError(f"{what}: dimension mismatch ({x.size} elements, expected {n})")
+    if writable and not x.flags.writeable:
+        raise ValueError(f"{what}: output array is read-only")
+    return x.ctypes.data
+
+
+def _as_host(x, dtype, shape):
+    """numpy input coerced like pybind11's forcecast (module.cpp:17)."""
+    if _is_torch(x):
+        return x
+    a = np.ascontiguousarray(x, dtype=dtype)
+    if a.shape != tuple(shape) and a.size == int(np.prod(shape)):
+        a = a.reshape(shape)
+    if a.shape != tuple(shape):
+        raise ValueError(f"dimension mismatch: got {a.shape}, expected {tuple(shape)}")
+    return a
+
+
+def _check_mask(m):
+    """mask_from_array (module.cpp:31-36): masks must be {0,1}."""
+    if isinstance(m, np.ndarray) and m.size and int(m.max()) > 1:
+        raise ValueError("mask values must be 0 or 1")
+
+
+# ------------------------------------------------------------------ configs
+
+@dataclass
+class MixtureConfig:
+    """MixtureConfig (mixture.hpp:16-26), defaults mixture.hpp:17-23."""
+
+    components: int = 3
+    learning_rate: float = 0.05
+    match_lambda: float = 2.5
+    background_threshold: float = 0.8
+    initial_sigma: float = 15.0
+    initial_weight: float = 0.05
+    variance_floor: float = 4.0
+
+    def _c(self) -> _lib.MixtureCfg:
+        return _lib.MixtureCfg(int(self.components), self.learning_rate, self.match_lambda,
+                               self.background_threshold, self.initial_sigma,
+                               self.initial_weight, self.variance_floor)
+
+    def validate(self):
+        """Raises ValueError like MixtureConfig::validate (mixture.cpp:9-24)."""
+        c = self._c()
+        check(lib.rgbdseg_mixture_validate(C.byref(c)))
+
+    def to_dict(self):
+        return {k: getattr(self, k) for k in (
+            "components", "learning_rate", "match_lambda", "background_threshold",
+            "initial_sigma", "initial_weight", "variance_floor")}
+
+
+@dataclass
+class RunConfig:
+    """The RunConfig fields on the hot path (processor.hpp:17-33)."""
+
+    color_gmm: MixtureConfig = field(default_factory=MixtureConfig)
+    depth_gmm: MixtureConfig = field(default_factory=MixtureConfig)
+    fusion_counter_limit: int = 3
+    fusion_initial_label: int = 0
+    warmup_frames: int = 30
+
+    @staticmethod
+    def defaults() -> "RunConfig":
+        """RunConfig::defaults (processor.cpp:35-43): depth adapts slower."""
+        c = RunConfig()
+        c.depth_gmm.learning_rate = 0.01
+        c.depth_gmm.initial_sigma = 100.0
+        return c
+
+    def to_json(self) -> str:
+        return json.dumps({
+            "color_gmm": self.color_gmm.to_dict(),
+            "depth_gmm": self.depth_gmm.to_dict(),
+            "fusion": {"counter_limit": self.fusion_counter_limit,
+                       "initial_label": self.fusion_initial_label},
+            "evaluation": {"warmup_frames": self.warmup_frames},
+        }, indent=2)
+
+
+def default_config_json() -> str:
+    """module.cpp:192 (hot-path subset of RunConfig::to_json)."""
+    return RunConfig.defaults().to_json()
+
+
+# ------------------------------------------------------------------ per pixel
+
+class PixelMixture:
+    """PixelMixture (mixture.hpp:30-41); read-only view like module.cpp:55-65."""
+
+    __slots__ = ("_rec",)
+
+    def __init__(self, rec: np.ndarray):
+        self._rec = rec  # one PIXEL_MIXTURE_DTYPE record (shape ())
+
+    @property
+    def components(self) -> int:
+        return int(self._rec["components"])
+
+    @property
+    def channels(self) -> int:
+        return int(self._rec["channels"])
+
+    @property
+    def weights(self):
+        return [float(x) for x in self._rec["weights"][: self.components]]
+
+    @property
+    def variances(self):
+        return [float(x) for x in self._rec["variances"][: self.components]]
+
+    @property
+    def means(self):
+        m, c = self.components, self.channels
+        return self._rec["means"][: m * c].reshape(m, c).tolist()
+
+    def raw(self) -> np.ndarray:
+        return self._rec
+
+    def __eq__(self, other):
+        return isinstance(other, PixelMixture) and self._rec.tobytes() == other._rec.tobytes()
+
+
+def init_mixtures(values, cfg: MixtureConfig, device: int = 0) -> np.ndarray:
+    """Batched init_mixture (mixture.cpp:58-72) on the GPU: values[n, C] ->
+    n PIXEL_MIXTURE_DTYPE records."""
+    v = np.ascontiguousarray(values, dtype=np.float32)
+    if v.ndim == 1:
+        v = v[None, :]
+    n, ch = v.shape
+    out = np.zeros(n, PIXEL_MIXTURE_DTYPE)
+    c = cfg._c()
+    check(lib.rgbdseg_init_mixtures(v.ctypes.data, ch, n, C.byref(c), out.ctypes.data, device))
+    return out
+
+
+def step_mixtures(recs: np.ndarray, values, cfg: MixtureConfig, device: int = 0) -> np.ndarray:
+    """Batched step_pixel (mixture.cpp:148-154) on the GPU, in place.
+    Returns uint8 labels (1 = Foreground)."""
+    if recs.dtype != PIXEL_MIXTURE_DTYPE or not recs.flags.c_contiguous:
+        raise ValueError("records must be a contiguous PIXEL_MIXTURE_DTYPE array")
+    v = np.ascontiguousarray(values, dtype=np.float32)
+    n = recs.size
+    if v.ndim == 1:
+        v = v.reshape(n, -1)
+    if v.shape[0] != n:
+        raise ValueError("one observation per record expected")
+    labels = np.empty(n, np.uint8)
+    c = cfg._c()
+    check(lib.rgbdseg_step_mixtures(recs.ctypes.data, v.ctypes.data, v.shape[1], n, C.byref(c),
+                                    labels.ctypes.data, device))
+    return labels
+
+
+def init_mixture(first_value, cfg: MixtureConfig) -> PixelMixture:
+    """init_mixture (module.cpp:67-69): list of 1..4 floats."""
+    v = np.asarray(list(first_value), dtype=np.float32)
+    if v.size < 1 or v.size > 4:
+        raise ValueError("init_mixture: bad observation dimensionality")
+    return PixelMixture(init_mixtures(v[None, :], cfg)[0:1].reshape(()))
+
+
+def step_pixel(mix: PixelMixture, value, cfg: MixtureConfig) -> int:
+    """step_pixel (module.cpp:70-73): updates `mix` in place, returns 1 = FG."""
+    v = np.asarray(list(value), dtype=np.float32)
+    if v.size != mix.channels:
+        raise ValueError("step_pixel: observation dimensionality does not match the mixture")
+    rec = mix._rec.reshape(1)
+    lab = step_mixtures(rec, v[None, :], cfg)
+    return int(lab[0])
+
+
+# ------------------------------------------------------------------ banks
+
+class BankMode:
+    Color3 = _lib.COLOR3
+    Depth1 = _lib.DEPTH1
+
+
+class ModelBank:
+    """Device-resident ModelBank (segmenter.hpp:25-55) over `streams` frames
+    of width x height.  Plane accessors return host copies (the reference
+    returns mutable Plane& references; use ``upload_plane`` to write)."""
+
+    def __init__(self, width: int, height: int, mode, cfg: MixtureConfig, streams: int = 1,
+                 device: int = 0, _borrowed=None):
+        if isinstance(mode, str):
+            mode = {"Color3": _lib.COLOR3, "Depth1": _lib.DEPTH1}[mode]
+        self.width, self.height, self.streams, self.mode = width, height, streams, mode
+        self.channels = 3 if mode == _lib.COLOR3 else 1
+        self.device = device
+        self._owner = None
+        if _borrowed is not None:
+            self._h, self._owner = _borrowed
+            self.components = lib.rgbdseg_bank_planes(self._h) // (self.channels + 2)
+            return
+        self.components = int(cfg.components)
+        h = C.c_void_p()
+        c = cfg._c()
+        check(lib.rgbdseg_bank_create(width, height, streams, mode, C.byref(c), device,
+                                      C.byref(h)), "ModelBank")
+        self._h = h.value
+
+    def __del__(self):
+        if getattr(self, "_h", None) and self._owner is None:
+            lib.rgbdseg_bank_destroy(self._h)
+            self._h = None
+
+    @property
+    def npx(self) -> int:
+        return self.width * self.height * self.streams
+
+    def _shape(self):
+        return (self.height, self.width) if self.streams == 1 else (
+            self.streams, self.height, self.width)
+
+    def plane_id_mean(self, i, c):
+        return i * self.channels + c
+
+    def plane_id_variance(self, i):
+        return self.components * self.channels + i
+
+    def plane_id_weight(self, i):
+        return self.components * self.channels + self.components + i
+
+    def download_plane(self, pid: int) -> np.ndarray:
+        dt = np.uint8 if pid == _lib.FLAGS_PLANE else np.float32
+        out = np.empty(self._shape(), dt)
+        check(lib.rgbdseg_bank_download(self._h, pid, out.ctypes.data))
+        return out
+
+    def upload_plane(self, pid: int, arr):
+        dt = np.uint8 if pid == _lib.FLAGS_PLANE else np.float32
+        a = _as_host(arr, dt, self._shape())
+        check(lib.rgbdseg_bank_upload(self._h, pid, _buf(a, dt, self.npx, "plane")))
+
+    def mean_plane(self, component: int, channel: int) -> np.ndarray:
+        return self.download_plane(self.plane_id_mean(component, channel))
+
+    def variance_plane(self, component: int) -> np.ndarray:
+        return self.download_plane(self.plane_id_variance(component))
+
+    def weight_plane(self, component: int) -> np.ndarray:
+        return self.download_plane(self.plane_id_weight(component))
+
+    def initialized_plane(self) -> np.ndarray:
+        return self.download_plane(_lib.FLAGS_PLANE)
+
+    def planes(self) -> np.ndarray:
+        """All float planes in ModelBank order, shape (M*C + 2M, npx)."""
+        P = lib.rgbdseg_bank_planes(self._h)
+        out = np.empty((P, self.npx), np.float32)
+        for p in range(P):
+            check(lib.rgbdseg_bank_download(self._h, p, out[p].ctypes.data))
+        return out
+
+    def gather(self, x: int, y: int, stream: int = 0) -> PixelMixture:
+        """ModelBank::gather (segmenter.cpp:36-47)."""
+        j = (stream * self.height + y) * self.width + x
+        P = self.planes()[:, j]
+        rec = np.zeros((), PIXEL_MIXTURE_DTYPE)
+        M, Ch = self.components, self.channels
+        rec["components"], rec["channels"] = M, Ch
+        rec["means"][: M * Ch] = P[: M * Ch]
+        rec["variances"][:M] = P[M * Ch: M * Ch + M]
+        rec["weights"][:M] = P[M * Ch + M:]
+        return PixelMixture(rec)
+
+    def is_initialized(self, x: int, y: int, stream: int = 0) -> bool:
+        return bool(self.initialized_plane().reshape(-1)[(stream * self.height + y) * self.width + x])
+
+    def state_equals(self, other: "ModelBank") -> bool:
+        """ModelBank::state_equals (segmenter.cpp:58-63), bitwise."""
+        return (self.width == other.width and self.height == other.height
+                and self.streams == other.streams and self.mode == other.mode
+                and self.components == other.components
+                and self.planes().tobytes() == other.planes().tobytes()
+                and np.array_equal(self.initialized_plane(), other.initialized_plane()))
+
+
+def _mask_out(out, n, shape):
+    if out is None:
+        return np.empty(shape, np.uint8), None
+    return out, out
+
+
+def segment_color(bank: ModelBank, r, g, b, cfg: MixtureConfig, workers: int = 1, out=None):
+    """segment_color (segmenter.cpp:107-119) on the GPU.  `workers` is
+    accepted for signature parity; the CUDA grid replaces the row split."""
+    shp = bank._shape()
+    r, g, b = (_as_host(x, np.uint8, shp) for x in (r, g, b))
+    mask, _ = _mask_out(out, bank.npx, shp)
+    c = cfg._c()
+    check(lib.rgbdseg_segment_color(bank._h, _buf(r, np.uint8, bank.npx, "segment_color(r)"),
+                                    _buf(g, np.uint8, bank.npx, "segment_color(g)"),
+                                    _buf(b, np.uint8, bank.npx, "segment_color(b)"), C.byref(c),
+                                    _buf(mask, np.uint8, bank.npx, "mask", True)))
+    return mask
+
+
+def segment_depth(bank: ModelBank, depth_mm, cfg: MixtureConfig, workers: int = 1, out=None):
+    """segment_depth (segmenter.cpp:121-131) on the GPU; raw 0 = no return."""
+    shp = bank._shape()
+    d = _as_host(depth_mm, np.uint16, shp)
+    mask, _ = _mask_out(out, bank.npx, shp)
+    c = cfg._c()
+    check(lib.rgbdseg_segment_depth(bank._h, _buf(d, np.uint16, bank.npx, "segment_depth"),
+                                    C.byref(c), _buf(mask, np.uint8, bank.npx, "mask", True)))
+    return mask
+
+
+# ------------------------------------------------------------------ fusion
+
+class FusionState:
+    """FusionState + reset_state + fuse_step (fusion.hpp:11-23, module.cpp:75-90)."""
+
+    def __init__(self, width: int, height: int, initial_label: int = 0, counter_limit: int = 3,
+                 streams: int = 1, device: int = 0, _borrowed=None):
+        self.width, self.height, self.streams = width, height, streams
+        self._owner = None
+        if _borrowed is not None:
+            self._h, self._owner = _borrowed
+            return
+        h = C.c_void_p()
+        check(lib.rgbdseg_fusion_create(width, height, streams, int(initial_label),
+                                        int(counter_limit), device, C.byref(h)), "FusionState")
+        self._h = h.value
+
+    def __del__(self):
+        if getattr(self, "_h", None) and self._owner is None:
+            lib.rgbdseg_fusion_destroy(self._h)
+            self._h = None
+
+    def _shape(self):
+        return (self.height, self.width) if self.streams == 1 else (
+            self.streams, self.height, self.width)
+
+    @property
+    def npx(self):
+        return self.width * self.height * self.streams
+
+    def step(self, rgb, depth, out=None):
+        shp = self._shape()
+        rgb, depth = _as_host(rgb, np.uint8, shp), _as_host(depth, np.uint8, shp)
+        _check_mask(rgb)
+        _check_mask(depth)
+        res, _ = _mask_out(out, self.npx, shp)
+        check(lib.rgbdseg_fusion_step(self._h, _buf(rgb, np.uint8, self.npx, "fuse_step(rgb)"),
+                                      _buf(depth, np.uint8, self.npx, "fuse_step(depth)"),
+                                      _buf(res, np.uint8, self.npx, "out", True)))
+        return res
+
+    @property
+    def out(self) -> np.ndarray:
+        o = np.empty(self._shape(), np.uint8)
+        check(lib.rgbdseg_fusion_download(self._h, o.ctypes.data, None))
+        return o
+
+    @property
+    def cpt(self) -> np.ndarray:
+        c = np.empty(self._shape(), np.int8)
+        check(lib.rgbdseg_fusion_download(self._h, None, c.ctypes.data))
+        return c
+
+    def upload(self, out=None, cpt=None):
+        shp = self._shape()
+        o = _as_host(out, np.uint8, shp) if out is not None else None
+        c = _as_host(cpt, np.int8, shp) if cpt is not None else None
+        check(lib.rgbdseg_fusion_upload(self._h, _buf(o, np.uint8, self.npx, "out"),
+                                        _buf(c, np.int8, self.npx, "cpt")))
+
+
+def fuse_step(state: FusionState, rgb_mask, depth_mask_registered):
+    """fuse_step (fusion.cpp:17-46): returns a copy of state.out."""
+    return state.step(rgb_mask, depth_mask_registered)
+
+
+def reset_state(width: int, height: int, initial_label: int = 0, counter_limit: int = 3):
+    """reset_state (fusion.cpp:7-15)."""
+    return FusionState(width, height, initial_label, counter_limit)
+
+
+# ------------------------------------------------------------------ processor
+
+@dataclass
+class FrameMasks:
+    """FrameMasks (processor.hpp:46-53) for the fused method."""
+
+    index: int
+    rgb: Optional[object] = None
+    depth: Optional[object] = None
+    fused: Optional[object] = None
+
+
+class SequenceProcessor:
+    """SequenceProcessor (processor.hpp:60-80) for the fused method on a
+    registered sequence, over `streams` independent camera streams batched
+    into one fused kernel per step."""
+
+    def __init__(self, width: int, height: int, config: Optional[RunConfig] = None,
+                 streams: int = 1, device: int = 0, variant: str = "auto", host_chunks: int = 0):
+        config = config or RunConfig.defaults()
+        self.width, self.height, self.streams, self.device = width, height, streams, device
+        self.config = config
+        pc = _lib.ProcessorCfg()
+        lib.rgbdseg_processor_defaults(C.byref(pc), width, height)
+        pc.streams = streams
+        pc.color = config.color_gmm._c()
+        pc.depth = config.depth_gmm._c()
+        pc.fusion_counter_limit = int(config.fusion_counter_limit)
+        pc.fusion_initial_label = int(config.fusion_initial_label)
+        pc.device = device
+        pc.host_chunks = host_chunks
+        h = C.c_void_p()
+        check(lib.rgbdseg_processor_create(C.byref(pc), C.byref(h)), "SequenceProcessor")
+        self._h = h.value
+        self.set_variant(variant)
+        self._color = ModelBank(width, height, _lib.COLOR3, None, streams, device,
+                                _borrowed=(lib.rgbdseg_processor_color_bank(self._h), self))
+        self._depth = ModelBank(width, height, _lib.DEPTH1, None, streams, device,
+                                _borrowed=(lib.rgbdseg_processor_depth_bank(self._h), self))
+        self._fusion = FusionState(width, height, streams=streams, device=device,
+                                   _borrowed=(lib.rgbdseg_processor_fusion(self._h), self))
+        self._keep = []
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.rgbdseg_processor_destroy(self._h)
+            self._h = None
+
+    @property
+    def npx(self):
+        return self.width * self.height * self.streams
+
+    def _shape(self):
+        return (self.height, self.width) if self.streams == 1 else (
+            self.streams, self.height, self.width)
+
+    def set_variant(self, variant: str):
+        check(lib.rgbdseg_processor_set_variant(self._h, _lib.VARIANTS[variant]))
+
+    def color_bank(self) -> ModelBank:
+        return self._color
+
+    def depth_bank(self) -> ModelBank:
+        return self._depth
+
+    def fusion_state(self) -> FusionState:
+        return self._fusion
+
+    @property
+    def stream_handle(self) -> int:
+        return lib.rgbdseg_processor_stream(self._h) or 0
+
+    @property
+    def frames(self) -> int:
+        return int(lib.rgbdseg_processor_frames(self._h))
+
+    def _args(self, r, g, b, depth, fused, rgb, dep):
+        shp, n = self._shape(), self.npx
+        r, g, b = (_as_host(x, np.uint8, shp) for x in (r, g, b))
+        depth = _as_host(depth, np.uint16, shp)
+        ptrs = [_buf(r, np.uint8, n, "process(r)"), _buf(g, np.uint8, n, "process(g)"),
+                _buf(b, np.uint8, n, "process(b)"), _buf(depth, np.uint16, n, "process(depth)"),
+                _buf(fused, np.uint8, n, "fused", True), _buf(rgb, np.uint8, n, "rgb", True),
+                _buf(dep, np.uint8, n, "depth_mask", True)]
+        return ptrs, (r, g, b, depth)
+
+    def process(self, r, g, b, depth, want=("rgb", "depth", "fused"), out=None) -> FrameMasks:
+        """SequenceProcessor::process (processor.cpp:158-184), synchronous.
+        `out` may map 'rgb'/'depth'/'fused' to preallocated arrays/tensors."""
+        out = dict(out or {})
+        shp = self._shape()
+        for k in want:
+            if k not in out:
+                out[k] = np.empty(shp, np.uint8)
+        ptrs, keep = self._args(r, g, b, depth, out.get("fused"), out.get("rgb"), out.get("depth"))
+        idx = self.frames
+        check(lib.rgbdseg_processor_process(self._h, *ptrs), "process")
+        return FrameMasks(idx, out.get("rgb"), out.get("depth"), out.get("fused"))
+
+    def submit(self, r, g, b, depth, fused=None, rgb=None, depth_mask=None):
+        """Enqueue one step without waiting; buffers must stay alive and
+        unmodified until ``sync()``."""
+        ptrs, keep = self._args(r, g, b, depth, fused, rgb, depth_mask)
+        self._keep.append((keep, fused, rgb, depth_mask))
+        check(lib.rgbdseg_processor_submit(self._h, *ptrs), "submit")
+
+    def sync(self):
+        check(lib.rgbdseg_processor_sync(self._h), "sync")
+        self._keep.clear()
+
+
+# ------------------------------------------------------------------ scenes
+
+def builtin_scenario_names():
+    return ["A", "B"]
+
+
+def render_scenario(name: str, width: int, height: int, frame: int, streams: int = 1,
+                    seed0: int = 1, device: int = 0, out=None, stream=None, with_gt=False):
+    """Render builtin scenario `name` (synthetic.cpp:234-273, render_frame
+    :119-195) for `streams` streams (seeds seed0..seed0+streams-1) straight
+    into CUDA tensors (torch is used only as the device allocator)."""
+    import torch
+
+    shp = (streams, height, width)
+    if out is None:
+        dev = torch.device("cuda", device)
+        out = {"r": torch.empty(shp, dtype=torch.uint8, device=dev),
+               "g": torch.empty(shp, dtype=torch.uint8, device=dev),
+               "b": torch.empty(shp, dtype=torch.uint8, device=dev),
+               "depth": torch.empty(shp, dtype=torch.uint16, device=dev)}
+        if with_gt:
+            out["gt"] = torch.empty(shp, dtype=torch.uint8, device=dev)
+    gt = out.get("gt")
+    check(lib.rgbdseg_render_scenario(name.encode()[:1], width, height, streams, seed0, frame,
+                                      out["r"].data_ptr(), out["g"].data_ptr(),
+                                      out["b"].data_ptr(), out["depth"].data_ptr(),
+                                      gt.data_ptr() if gt is not None else None, device,
+                                      stream), "render_scenario")
+    return out

@@ -1,0 +1,109 @@
+"""CPU tests of the drop-in boundary: the C-ABI library loads, exports every
+symbol include/rgbdseg_c.h declares, and validates like the reference
+(std::invalid_argument <-> RGBDSEG_EINVAL <-> ValueError) without a GPU."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "rgbdseg_c.h")
+LIB = os.path.join(ROOT, "paper_2110_14934_b200", "librgbdseg_b200.so")
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(rgbdseg_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_declares_the_boundary():
+    names = declared_functions()
+    for must in ("rgbdseg_segment_color", "rgbdseg_segment_depth", "rgbdseg_fusion_step",
+                 "rgbdseg_processor_process", "rgbdseg_step_mixtures", "rgbdseg_bank_download"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol():
+    lib = C.CDLL(LIB)
+    missing = [n for n in declared_functions() if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_python_binding_covers_every_declared_symbol():
+    from paper_2110_14934_b200 import _lib
+
+    assert set(declared_functions()) <= set(_lib.SIGNATURES)
+
+
+def test_library_is_sm100a_only():
+    out = subprocess.run(["cuobjdump", "--list-elf", LIB], capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr
+    arches = set(re.findall(r"sm_\d+a?", out.stdout))
+    assert arches == {"sm_100a"}, arches
+
+
+def test_hot_kernels_have_no_contracted_fma(tmp_path):
+    """The GMM arithmetic must not contract a*b+c (FMA
+    changes 32% of parameter words).  IEEE div/sqrt are single PTX ops
+    (div.rn / sqrt.rn) whose FFMA expansion is exact by construction, so
+    the PTX of every kernel must hold no fma.*.f32 at all."""
+    ptx = tmp_path / "k.ptx"
+    src = os.path.join(ROOT, "paper_2110_14934_b200", "csrc", "rgbdseg_kernels.cu")
+    r = subprocess.run(["nvcc", "-arch=sm_100a", "-ptx", "-std=c++17", "-fmad=false",
+                        "-prec-div=true", "-prec-sqrt=true", "-ftz=false", src, "-o", str(ptx)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    text = ptx.read_text()
+    assert "k_fused_ldg" in text
+    assert re.search(r"\bfma\.[a-z]+\.f32", text) is None
+    assert "div.rn.f32" in text and "sqrt.rn.f32" in text
+    assert ".ftz.f32" not in text  # (libdevice f64 helpers of the scene generator use rcp.approx.ftz.f64)
+
+
+def test_config_validation_messages():
+    import paper_2110_14934_b200 as R
+
+    R.MixtureConfig().validate()
+    cases = [
+        (dict(components=6), "components must be in [3,5]"),
+        (dict(components=2), "components must be in [3,5]"),
+        (dict(learning_rate=1.5), "learning_rate must be in (0,1)"),
+        (dict(background_threshold=0.0), "background_threshold must be in (0,1)"),
+        (dict(match_lambda=-1.0), "match_lambda must be positive"),
+        (dict(initial_sigma=0.0), "initial_sigma must be positive"),
+        (dict(initial_weight=1.0), "initial_weight must be in (0,1)"),
+        (dict(variance_floor=0.0), "variance_floor must be positive"),
+    ]
+    for kw, msg in cases:
+        with pytest.raises(ValueError, match=re.escape(msg)):
+            R.MixtureConfig(**kw).validate()
+
+
+def test_invalid_handles_rejected_before_touching_a_gpu():
+    import paper_2110_14934_b200 as R
+
+    with pytest.raises(ValueError, match="components"):
+        R.ModelBank(8, 8, "Color3", R.MixtureConfig(components=7))
+    with pytest.raises(ValueError, match="non-positive"):
+        R.ModelBank(0, 8, "Color3", R.MixtureConfig())
+    with pytest.raises(ValueError, match="counter_limit"):
+        R.FusionState(4, 4, counter_limit=0)
+    with pytest.raises(ValueError, match="label must be 0 or 1"):
+        R.FusionState(4, 4, initial_label=2)
+    with pytest.raises(ValueError, match="dimensionality"):
+        R.init_mixture([], R.MixtureConfig())
+
+
+def test_default_config_json_matches_reference_defaults():
+    import json
+
+    import paper_2110_14934_b200 as R
+
+    cfg = json.loads(R.default_config_json())
+    assert cfg["color_gmm"]["components"] == 3
+    assert cfg["depth_gmm"]["learning_rate"] == pytest.approx(0.01)
+    assert cfg["depth_gmm"]["initial_sigma"] == 100.0
+    assert cfg["fusion"] == {"counter_limit": 3, "initial_label": 0}
