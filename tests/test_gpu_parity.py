@@ -226,7 +226,7 @@ def test_fusion_truth_table(R):
 
 # ------------------------------------------------------------ fused processor (K1)
 
-@pytest.mark.parametrize("variant", ["ldg", "ldg_elide"])
+@pytest.mark.parametrize("variant", ["ldg", "ldg_elide", "bulk", "bulk_elide"])
 @pytest.mark.parametrize("name", [s[0] for s in SCENARIOS])
 def test_processor_scenarios_match_reference_golden(R, port, name, variant):
     """The fused kernel over whole golden sequences: every per-frame rgb /
@@ -250,7 +250,7 @@ def test_processor_scenarios_match_reference_golden(R, port, name, variant):
     assert sha256(db.planes(), db.initialized_plane()) == gold["depth_bank"]
 
 
-@pytest.mark.parametrize("variant", ["ldg", "ldg_elide"])
+@pytest.mark.parametrize("variant", ["ldg", "ldg_elide", "bulk", "bulk_elide"])
 def test_processor_multistream_device_vs_oracle(R, port, cuda, variant):
     """Config-4 shape in miniature: S streams (seeds 1..S) batched in one
     kernel over device-resident frames rendered by the GPU scene generator,
@@ -361,3 +361,42 @@ def test_8k_frame_sampled_exact_and_chunk_invariant(R, port, cuda):
     assert P.tobytes() == orc.color.planes().tobytes()
     del dev
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("variant", ["auto", "bulk", "bulk_elide"])
+def test_processor_tail_and_misaligned_inputs(R, port, cuda, variant):
+    """Odd frame sizes (a 32-pixel-chunk tail handled by the LDG kernel) and
+    device planes that are not 16-byte aligned (bulk copies impossible ->
+    LDG fallback) give the oracle's bits."""
+    import torch
+
+    w, h, S, M = 37, 23, 3, 4
+    cfg = R.RunConfig.defaults()
+    cfg.color_gmm.components = cfg.depth_gmm.components = M
+    proc = R.SequenceProcessor(w, h, cfg, streams=S, variant=variant)
+    orc = [O.PortProcessor(port, w * h, O.color_cfg(M), O.depth_cfg(M)) for _ in range(S)]
+    rng = np.random.default_rng(1)
+    n = S * w * h
+    for f in range(30):
+        base = rng.integers(0, 256, 3, dtype=np.uint8)
+        host = {k: np.clip(base[i] + rng.integers(-6, 7, (S, h, w)), 0, 255).astype(np.uint8)
+                for i, k in enumerate("rgb")}
+        host["depth"] = (2000 + rng.integers(-30, 31, (S, h, w))).astype(np.uint16)
+        host["depth"][:, 2:5, 3:9] = 0
+        dev = {}
+        for k, v in host.items():  # misaligned on odd frames: offset the view by one element
+            off = f % 2
+            t = torch.zeros(n + 8, dtype=torch.int16 if v.dtype == np.uint16 else torch.uint8,
+                            device=cuda)
+            src = torch.from_numpy(v.view(np.int16) if v.dtype == np.uint16 else v).reshape(-1)
+            t[off:off + n] = src.to(cuda)
+            dev[k] = t[off:off + n].view(torch.uint16 if v.dtype == np.uint16 else torch.uint8)
+        fused = torch.empty(n, dtype=torch.uint8, device=cuda)
+        proc.process(dev["r"], dev["g"], dev["b"], dev["depth"], want=(), out={"fused": fused})
+        got = fused.cpu().numpy().reshape(S, -1)
+        for s in range(S):
+            _, _, fu = orc[s].process(host["r"][s], host["g"][s], host["b"][s], host["depth"][s])
+            assert np.array_equal(got[s], fu), (f, s)
+    P = proc.depth_bank().planes().reshape(-1, S, w * h)
+    for s in range(S):
+        assert P[:, s].tobytes() == orc[s].depth.planes().tobytes()
