@@ -10,7 +10,7 @@ NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -fmad=false -prec-div=true -prec-sq
 PKG      := paper_2110_14934_b200
 CSRC     := $(PKG)/csrc
 LIB      := $(PKG)/librgbdseg_b200.so
-OBJS     := $(CSRC)/rgbdseg_kernels.o $(CSRC)/rgbdseg_bulk.o $(CSRC)/rgbdseg_capi.o
+OBJS     := $(CSRC)/rgbdseg_kernels.o $(CSRC)/rgbdseg_capi.o
 
 all: lib oracle
 

@@ -223,7 +223,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="streams256", choices=sorted(WORKLOADS))
-    ap.add_argument("--variant", default="auto", choices=["auto", "ldg", "ldg_elide"])
+    ap.add_argument("--variant", default="auto",
+                    choices=["auto", "ldg", "ldg_elide"])
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)

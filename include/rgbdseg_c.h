@@ -170,10 +170,9 @@ rgbdseg_fusion* rgbdseg_processor_fusion(rgbdseg_processor* p);
 /* The CUDA stream the processor's kernels run on (cudaStream_t as void*),
  * so callers can time the kernels with events on the launching stream. */
 void* rgbdseg_processor_stream(rgbdseg_processor* p);
-/* Kernel variant: 0 = auto (TMA bulk + write elision when the planes are
- * 16-byte aligned, else LDG), 1 = LDG one pixel per thread, 2 = LDG with
- * write elision, 3 = TMA bulk dense write-back, 4 = TMA bulk + elision.
- * Every variant produces the same bits; they differ only in HBM traffic. */
+/* Kernel variant: 0 = auto (= 2), 1 = dense write-back of every state word,
+ * 2 = write elision (words whose bits did not change are not rewritten).
+ * Every variant produces the same bits; they differ only in HBM writes. */
 int rgbdseg_processor_set_variant(rgbdseg_processor* p, int variant);
 
 /* ---- synthetic scenes on the GPU (synthetic.cpp:119-195, harness) ------

@@ -15,7 +15,7 @@ LIB_PATH = os.environ.get("RGBDSEG_B200_LIB", os.path.join(HERE, "librgbdseg_b20
 OK, EINVAL, ECUDA, ENOMEM, ERUNTIME = 0, 1, 2, 3, 4
 COLOR3, DEPTH1 = 0, 1
 FLAGS_PLANE = -1
-VARIANTS = {"auto": 0, "ldg": 1, "ldg_elide": 2, "bulk": 3, "bulk_elide": 4}
+VARIANTS = {"auto": 0, "ldg": 1, "ldg_elide": 2}
 
 
 class MixtureCfg(C.Structure):

@@ -710,7 +710,7 @@ rgbdseg_fusion* rgbdseg_processor_fusion(rgbdseg_processor* p) { return p->fusio
 void* rgbdseg_processor_stream(rgbdseg_processor* p) { return (void*)p->sc; }
 
 int rgbdseg_processor_set_variant(rgbdseg_processor* p, int variant) {
-    if (variant < kAuto || variant > kBulkElide) return fail(RGBDSEG_EINVAL, "unknown kernel variant");
+    if (variant < kAuto || variant > kLdgElide) return fail(RGBDSEG_EINVAL, "unknown kernel variant");
     p->variant = variant;
     return RGBDSEG_OK;
 }

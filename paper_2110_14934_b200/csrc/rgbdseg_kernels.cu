@@ -419,29 +419,7 @@ cudaError_t fused_ldg_md(const FusedArgs& a, bool elide, cudaStream_t s) {
 
 template <int MC, int MD>
 cudaError_t fused_md(const FusedArgs& a, int variant, cudaStream_t s) {
-    if (a.n == 0) return cudaSuccess;
-    const bool bulk = (variant == kAuto || variant == kBulk || variant == kBulkElide) &&
-                      bulk_eligible(a);
-    const bool elide = variant == kAuto || variant == kLdgElide || variant == kBulkElide;
-    if (!bulk) return fused_ldg_md<MC, MD>(a, elide, s);
-    cudaError_t e = launch_fused_bulk(a, elide, s);
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-    if (e != cudaSuccess) return e;
-    const size_t full = a.n & ~size_t(31);
-    if (full == a.n) return cudaSuccess;
-    FusedArgs t = a;  // the n % 32 tail through the LDG kernel
-    t.r += full;
-    t.g += full;
-    t.b += full;
-    t.d += full;
-    if (t.rgb_mask) t.rgb_mask += full;
-    if (t.depth_mask) t.depth_mask += full;
-    if (t.fused_copy) t.fused_copy += full;
-    t.out += full;
-    t.cpt += full;
-    t.base += full;
-    t.n = a.n - full;
-    return fused_ldg_md<MC, MD>(t, elide, s);
+    return fused_ldg_md<MC, MD>(a, variant != kLdgDense, s);
 }
 
 template <int MC>

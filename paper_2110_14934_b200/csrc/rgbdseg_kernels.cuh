@@ -43,13 +43,10 @@ struct FusedArgs {
     int limit;
 };
 
-// Kernel variants of K1.  Auto = bulk with write elision when the pointers
-// allow it (16-byte aligned planes), else LDG.
-enum Variant { kAuto = 0, kLdgDense = 1, kLdgElide = 2, kBulk = 3, kBulkElide = 4 };
-
-// TMA-bulk K1 (rgbdseg_bulk.cu) over the full 32-pixel chunks of a launch.
-bool bulk_eligible(const FusedArgs& a);
-cudaError_t launch_fused_bulk(const FusedArgs& a, bool elide, cudaStream_t s);
+// Kernel variants of K1 (identical results; they differ in HBM writes).
+// Auto = LDG with write elision.  A TMA cp.async.bulk staging variant was
+// measured and dropped (profiles/variants_r01.json).
+enum Variant { kAuto = 0, kLdgDense = 1, kLdgElide = 2 };
 
 // All launchers return cudaGetLastError() after the launch.
 cudaError_t launch_fused(const FusedArgs& a, int variant, cudaStream_t s);
