@@ -92,23 +92,29 @@ int rgbdseg_step_mixtures(rgbdseg_pixel_mixture* mix, const float* values, int c
                           size_t n, const rgbdseg_mixture_cfg* cfg, uint8_t* labels, int device);
 
 /* ---- ModelBank: segmenter.hpp:25-55 ------------------------------------
- * Device-resident SoA bank over `npx` = width*height*streams pixels.
- * Plane ids (ModelBank plane order, segmenter.hpp:51-54):
- *   mean(i,c) = i*C + c ; variance(i) = M*C + i ; weight(i) = M*C + M + i ;
- *   the initialised-flag plane (uint8) is plane id RGBDSEG_FLAGS_PLANE.   */
+ * Device-resident bank over `npx` = width*height*streams pixels (streams
+ * back to back).  Plane ids follow ModelBank's plane order
+ * (segmenter.hpp:51-54): mean(i,c) = i*C + c ; variance(i) = M*C + i ;
+ * weight(i) = M*C + M + i ; the initialised-flag plane (uint8) is
+ * RGBDSEG_FLAGS_PLANE.  In HBM the planes are TILED: blocks of 32 pixels,
+ * each holding the 32 values of every plane in turn, then the 32 flag bytes
+ * in a 128-byte slot -- see rgbdseg_bank_device_ptrs. */
 #define RGBDSEG_FLAGS_PLANE (-1)
 int rgbdseg_bank_create(int width, int height, int streams, int mode,
                         const rgbdseg_mixture_cfg* cfg, int device, rgbdseg_bank** out);
 void rgbdseg_bank_destroy(rgbdseg_bank* bank);
 int rgbdseg_bank_planes(const rgbdseg_bank* bank); /* M*C + 2M */
-/* Copy one plane (npx elements; float, or uint8 for the flag plane) out of /
- * into the bank.  Backs gather/scatter/mean_plane/state_equals. */
+/* Copy one flat plane (npx elements; float, or uint8 for the flag plane;
+ * host or device memory) out of / into the bank.  Backs mean_plane /
+ * variance_plane / weight_plane / initialized_plane, gather/scatter and
+ * state_equals (segmenter.hpp:33-46). */
 int rgbdseg_bank_download(const rgbdseg_bank* bank, int plane, void* dst);
 int rgbdseg_bank_upload(rgbdseg_bank* bank, int plane, const void* src);
-/* Device base pointer of the state planes / the flag plane, and the plane
- * pitch in elements (>= npx, padded for 128-byte alignment). */
-int rgbdseg_bank_device_ptrs(const rgbdseg_bank* bank, float** state, uint8_t** flags,
-                             size_t* pitch);
+/* Raw tiled storage: `nblocks` blocks of `block_bytes` = (planes+1)*128
+ * bytes; value of plane p for pixel j is float[(j/32)*(block_bytes/4) +
+ * p*32 + j%32], its flag byte is at float offset planes*32 of the block. */
+int rgbdseg_bank_device_ptrs(const rgbdseg_bank* bank, void** tiles, size_t* block_bytes,
+                             size_t* nblocks);
 
 /* segment_color, segmenter.cpp:107-119 / segment_depth, :121-131.
  * Planes are npx elements, row-major, streams back to back.  mask_out may be

@@ -69,7 +69,7 @@ SIGNATURES = {
     "rgbdseg_bank_planes": (_i, [_vp]),
     "rgbdseg_bank_download": (_i, [_vp, _i, _vp]),
     "rgbdseg_bank_upload": (_i, [_vp, _i, _vp]),
-    "rgbdseg_bank_device_ptrs": (_i, [_vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_sz)]),
+    "rgbdseg_bank_device_ptrs": (_i, [_vp, C.POINTER(_vp), C.POINTER(_sz), C.POINTER(_sz)]),
     "rgbdseg_segment_color": (_i, [_vp, _vp, _vp, _vp, C.POINTER(MixtureCfg), _vp]),
     "rgbdseg_segment_depth": (_i, [_vp, _vp, C.POINTER(MixtureCfg), _vp]),
     "rgbdseg_fusion_create": (_i, [_i, _i, _i, _i, _i, _i, C.POINTER(_vp)]),

@@ -154,13 +154,12 @@ int stage_in(const void* src, size_t bytes, Scratch& scratch, const void** dev, 
 // ============================================================== handles
 struct rgbdseg_bank {
     int width, height, streams, mode, M, C, device;
-    size_t npx, pitch;
+    size_t npx, nblocks;
     rgbdseg_mixture_cfg cfg;
-    float* state = nullptr;
-    uint8_t* flags = nullptr;
+    float* state = nullptr;  // tiled: nblocks * bank_stride(M, C) floats
     cudaStream_t stream = nullptr;
-    Scratch s_r, s_g, s_b, s_mask;
-    BankView view() const { return BankView{state, flags, pitch, M, C}; }
+    Scratch s_r, s_g, s_b, s_mask, s_plane;
+    BankView view() const { return BankView{state, M, C}; }
 };
 
 struct rgbdseg_fusion {
@@ -297,10 +296,8 @@ int rgbdseg_bank_create(int width, int height, int streams, int mode,
     b->device = device;
     b->cfg = *cfg;
     b->npx = (size_t)width * height * streams;
-    b->pitch = pitch_for(b->npx);
-    const size_t planes = (size_t)b->M * b->C + 2 * b->M;
-    int rc = dalloc(&b->state, planes * b->pitch);
-    if (!rc) rc = dalloc(&b->flags, b->pitch);
+    b->nblocks = (b->npx + kBlockPx - 1) / kBlockPx;
+    int rc = dalloc(&b->state, b->nblocks * (size_t)bank_stride(b->M, b->C));
     if (!rc) {
         cudaError_t e = cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking);
         if (e == cudaSuccess) e = launch_bank_reset(b->view(), cfg->initial_sigma, b->npx, b->stream);
@@ -320,47 +317,51 @@ void rgbdseg_bank_destroy(rgbdseg_bank* b) {
     DeviceGuard g(b->device);
     if (b->stream) cudaStreamSynchronize(b->stream);
     dfree(b->state);
-    dfree(b->flags);
     if (b->stream) cudaStreamDestroy(b->stream);
     delete b;
 }
 
 int rgbdseg_bank_planes(const rgbdseg_bank* b) { return b->M * b->C + 2 * b->M; }
 
-int rgbdseg_bank_device_ptrs(const rgbdseg_bank* b, float** state, uint8_t** flags,
-                             size_t* pitch) {
-    if (state) *state = b->state;
-    if (flags) *flags = b->flags;
-    if (pitch) *pitch = b->pitch;
+int rgbdseg_bank_device_ptrs(const rgbdseg_bank* b, void** tiles, size_t* block_bytes,
+                             size_t* nblocks) {
+    if (tiles) *tiles = b->state;
+    if (block_bytes) *block_bytes = (size_t)bank_stride(b->M, b->C) * sizeof(float);
+    if (nblocks) *nblocks = b->nblocks;
+    return RGBDSEG_OK;
+}
+
+// Flat plane <-> tiled bank through a gather/scatter kernel (device
+// destinations directly, host ones through a device scratch plane).
+static int bank_xfer(rgbdseg_bank* b, int plane, void* dst, const void* src) {
+    if (plane != RGBDSEG_FLAGS_PLANE && (plane < 0 || plane >= rgbdseg_bank_planes(b)))
+        return fail(RGBDSEG_EINVAL, "bank plane id out of range");
+    const size_t bytes = b->npx * (plane == RGBDSEG_FLAGS_PLANE ? 1 : sizeof(float));
+    const int pid = plane == RGBDSEG_FLAGS_PLANE ? -1 : plane;
+    void* dev = const_cast<void*>(dst ? dst : src);
+    const bool direct = on_device(dev);
+    if (!direct) {
+        if (int rc = b->s_plane.get(bytes, &dev)) return rc;
+        if (src) CU(cudaMemcpyAsync(dev, src, bytes, cudaMemcpyDefault, b->stream));
+    }
+    if (dst) {
+        CU(launch_bank_gather(b->view(), pid, b->npx, dev, b->stream));
+        if (!direct) CU(cudaMemcpyAsync(dst, dev, bytes, cudaMemcpyDefault, b->stream));
+    } else {
+        CU(launch_bank_scatter(b->view(), pid, b->npx, dev, b->stream));
+    }
+    CU(cudaStreamSynchronize(b->stream));
     return RGBDSEG_OK;
 }
 
 int rgbdseg_bank_download(const rgbdseg_bank* b, int plane, void* dst) {
     GUARD(b->device);
-    CU(cudaStreamSynchronize(b->stream));
-    if (plane == RGBDSEG_FLAGS_PLANE) {
-        CU(cudaMemcpy(dst, b->flags, b->npx, cudaMemcpyDefault));
-        return RGBDSEG_OK;
-    }
-    if (plane < 0 || plane >= rgbdseg_bank_planes(b))
-        return fail(RGBDSEG_EINVAL, "bank plane id out of range");
-    CU(cudaMemcpy(dst, b->state + (size_t)plane * b->pitch, b->npx * sizeof(float),
-                  cudaMemcpyDefault));
-    return RGBDSEG_OK;
+    return bank_xfer(const_cast<rgbdseg_bank*>(b), plane, dst, nullptr);
 }
 
 int rgbdseg_bank_upload(rgbdseg_bank* b, int plane, const void* src) {
     GUARD(b->device);
-    CU(cudaStreamSynchronize(b->stream));
-    if (plane == RGBDSEG_FLAGS_PLANE) {
-        CU(cudaMemcpy(b->flags, src, b->npx, cudaMemcpyDefault));
-        return RGBDSEG_OK;
-    }
-    if (plane < 0 || plane >= rgbdseg_bank_planes(b))
-        return fail(RGBDSEG_EINVAL, "bank plane id out of range");
-    CU(cudaMemcpy(b->state + (size_t)plane * b->pitch, src, b->npx * sizeof(float),
-                  cudaMemcpyDefault));
-    return RGBDSEG_OK;
+    return bank_xfer(b, plane, nullptr, src);
 }
 
 // run_bank's checks (segmenter.cpp:73-75) + mode checks (:109,:123).

@@ -41,33 +41,41 @@ __device__ __forceinline__ void st_stream(T* p, T v) {
     __stcs(p, v);
 }
 
+// Per-thread base of pixel j in a tiled bank; plane p is at +p*32 floats.
 template <int M, int C>
-__device__ __forceinline__ void load_mix(const BankView& bk, size_t j, Mixture<M, C>& m) {
-    const float* s = bk.state + j;
-    const size_t P = bk.pitch;
+__device__ __forceinline__ float* px_base(const BankView& bk, size_t j) {
+    return bk.state + (j / kBlockPx) * bank_stride(M, C) + (j % kBlockPx);
+}
+template <int M, int C>
+__device__ __forceinline__ uint8_t* px_flag(const BankView& bk, size_t j) {
+    return reinterpret_cast<uint8_t*>(bk.state + (j / kBlockPx) * bank_stride(M, C) +
+                                      bank_planes(M, C) * kBlockPx) +
+           (j % kBlockPx);
+}
+
+template <int M, int C>
+__device__ __forceinline__ void load_mix(const float* s, Mixture<M, C>& m) {
 #pragma unroll
     for (int i = 0; i < M; ++i)
 #pragma unroll
-        for (int c = 0; c < C; ++c) m.mu[i][c] = ld_stream(s + (size_t)(i * C + c) * P);
+        for (int c = 0; c < C; ++c) m.mu[i][c] = ld_stream(s + (i * C + c) * kBlockPx);
 #pragma unroll
-    for (int i = 0; i < M; ++i) m.var[i] = ld_stream(s + (size_t)(M * C + i) * P);
+    for (int i = 0; i < M; ++i) m.var[i] = ld_stream(s + (M * C + i) * kBlockPx);
 #pragma unroll
-    for (int i = 0; i < M; ++i) m.w[i] = ld_stream(s + (size_t)(M * C + M + i) * P);
+    for (int i = 0; i < M; ++i) m.w[i] = ld_stream(s + (M * C + M + i) * kBlockPx);
 }
 
 // Dense store of every plane (ModelBank::scatter, segmenter.cpp:49-56).
 template <int M, int C>
-__device__ __forceinline__ void store_mix(const BankView& bk, size_t j, const Mixture<M, C>& m) {
-    float* s = bk.state + j;
-    const size_t P = bk.pitch;
+__device__ __forceinline__ void store_mix(float* s, const Mixture<M, C>& m) {
 #pragma unroll
     for (int i = 0; i < M; ++i)
 #pragma unroll
-        for (int c = 0; c < C; ++c) st_stream(s + (size_t)(i * C + c) * P, m.mu[i][c]);
+        for (int c = 0; c < C; ++c) st_stream(s + (i * C + c) * kBlockPx, m.mu[i][c]);
 #pragma unroll
-    for (int i = 0; i < M; ++i) st_stream(s + (size_t)(M * C + i) * P, m.var[i]);
+    for (int i = 0; i < M; ++i) st_stream(s + (M * C + i) * kBlockPx, m.var[i]);
 #pragma unroll
-    for (int i = 0; i < M; ++i) st_stream(s + (size_t)(M * C + M + i) * P, m.w[i]);
+    for (int i = 0; i < M; ++i) st_stream(s + (M * C + M + i) * kBlockPx, m.w[i]);
 }
 
 // Elided store: identical memory image to store_mix, but words whose bits
@@ -75,42 +83,52 @@ __device__ __forceinline__ void store_mix(const BankView& bk, size_t j, const Mi
 // mean and variance can change in a step (mixture.cpp:105-113, 125-128); the
 // weights are compared individually.  touched < 0 means "all" (init).
 template <int M, int C>
-__device__ __forceinline__ void store_mix_elide(const BankView& bk, size_t j,
-                                                const Mixture<M, C>& m, int touched,
+__device__ __forceinline__ void store_mix_elide(float* s, const Mixture<M, C>& m, int touched,
                                                 const float (&w_old)[M]) {
-    float* s = bk.state + j;
-    const size_t P = bk.pitch;
 #pragma unroll
     for (int i = 0; i < M; ++i) {
         if (touched < 0 || touched == i) {
 #pragma unroll
-            for (int c = 0; c < C; ++c) st_stream(s + (size_t)(i * C + c) * P, m.mu[i][c]);
-            st_stream(s + (size_t)(M * C + i) * P, m.var[i]);
+            for (int c = 0; c < C; ++c) st_stream(s + (i * C + c) * kBlockPx, m.mu[i][c]);
+            st_stream(s + (M * C + i) * kBlockPx, m.var[i]);
         }
     }
 #pragma unroll
     for (int i = 0; i < M; ++i)
         if (touched < 0 || __float_as_uint(m.w[i]) != __float_as_uint(w_old[i]))
-            st_stream(s + (size_t)(M * C + M + i) * P, m.w[i]);
+            st_stream(s + (M * C + M + i) * kBlockPx, m.w[i]);
 }
 
-// run_bank's per-pixel body (segmenter.cpp:80-96) on a loaded mixture.
-// Returns the label; `touched` reports what changed for the elided store.
+// run_bank's per-pixel body (segmenter.cpp:80-96) on a mixture loaded from
+// `src`.  The branch-free fast step runs first; a pixel whose operands leave
+// its exact ranges (gmm_pixel.cuh) is reloaded and replayed by the generic
+// step, so the result is bit-identical either way.  `touched` reports what
+// changed for the elided store.
 template <int M, int C>
-__device__ __forceinline__ uint32_t bank_pixel(Mixture<M, C>& m, const float (&v)[C],
-                                               bool initialised, const MixCfg& k,
-                                               int& touched) {
+__device__ __forceinline__ uint32_t bank_pixel(Mixture<M, C>& m, const float* src,
+                                               const float (&v)[C], bool initialised,
+                                               const MixCfg& k, int& touched) {
     if (!initialised) {
         gmm_init(m, v, k);
         touched = -1;
         return 0u;
     }
-    return gmm_step(m, v, k, touched);
+    bool ok = true;
+    uint32_t label = gmm_step_fast(m, v, k, touched, ok);
+    if (!ok) {
+        load_mix(src, m);
+        label = gmm_step(m, v, k, touched);
+    }
+    return label;
 }
 
 // ---------------------------------------------------------------- K1 fused
 template <int MC, int MD, bool kElide>
-__global__ void __launch_bounds__(kThreads) k_fused_ldg(const __grid_constant__ FusedArgs a) {
+#ifndef RGBDSEG_FUSED_MIN_BLOCKS
+#define RGBDSEG_FUSED_MIN_BLOCKS 3
+#endif
+__global__ void __launch_bounds__(kThreads, RGBDSEG_FUSED_MIN_BLOCKS)
+    k_fused_ldg(const __grid_constant__ FusedArgs a) {
     const size_t i = (size_t)blockIdx.x * kThreads + threadIdx.x;
     if (i >= a.n) return;
     const size_t j = a.base + i;
@@ -120,26 +138,30 @@ __global__ void __launch_bounds__(kThreads) k_fused_ldg(const __grid_constant__ 
     const float vc[3] = {(float)ld_stream(a.r + i), (float)ld_stream(a.g + i),
                          (float)ld_stream(a.b + i)};
     const uint32_t raw = ld_stream(a.d + i);
-    const bool cinit = ld_stream(a.color.flags + j) != 0;
-    const bool dinit = ld_stream(a.depth.flags + j) != 0;
+    float* cs = px_base<MC, 3>(a.color, j);
+    float* ds = px_base<MD, 1>(a.depth, j);
+    uint8_t* cfl = px_flag<MC, 3>(a.color, j);
+    uint8_t* dfl = px_flag<MD, 1>(a.depth, j);
+    const bool cinit = ld_stream(cfl) != 0;
+    const bool dinit = ld_stream(dfl) != 0;
     const uint32_t out0 = ld_stream(a.out + i);
     const int cpt0 = (int)ld_stream(a.cpt + i);
     Mixture<MC, 3> cm;
     Mixture<MD, 1> dm;
-    load_mix(a.color, j, cm);
-    load_mix(a.depth, j, dm);
+    load_mix(cs, cm);
+    load_mix(ds, dm);
 
     // ---- colour stream (segment_color) ----
     float cw_old[MC];
 #pragma unroll
     for (int q = 0; q < MC; ++q) cw_old[q] = cm.w[q];
     int ct = 0;
-    const uint32_t lc = bank_pixel(cm, vc, cinit, a.ck, ct);
+    const uint32_t lc = bank_pixel(cm, cs, vc, cinit, a.ck, ct);
     if (kElide)
-        store_mix_elide(a.color, j, cm, ct, cw_old);
+        store_mix_elide(cs, cm, ct, cw_old);
     else
-        store_mix(a.color, j, cm);
-    if (!cinit) st_stream(a.color.flags + j, (uint8_t)1);
+        store_mix(cs, cm);
+    if (!cinit) st_stream(cfl, (uint8_t)1);
 
     // ---- depth stream (segment_depth): raw 0 = no return ----
     uint32_t ld = 0;
@@ -149,12 +171,12 @@ __global__ void __launch_bounds__(kThreads) k_fused_ldg(const __grid_constant__ 
 #pragma unroll
         for (int q = 0; q < MD; ++q) dw_old[q] = dm.w[q];
         int dt = 0;
-        ld = bank_pixel(dm, vd, dinit, a.dk, dt);
+        ld = bank_pixel(dm, ds, vd, dinit, a.dk, dt);
         if (kElide)
-            store_mix_elide(a.depth, j, dm, dt, dw_old);
+            store_mix_elide(ds, dm, dt, dw_old);
         else
-            store_mix(a.depth, j, dm);
-        if (!dinit) st_stream(a.depth.flags + j, (uint8_t)1);
+            store_mix(ds, dm);
+        if (!dinit) st_stream(dfl, (uint8_t)1);
     }
 
     // ---- List-1 fusion on the registered depth mask ----
@@ -177,13 +199,15 @@ __global__ void __launch_bounds__(kThreads)
     const size_t j = (size_t)blockIdx.x * kThreads + threadIdx.x;
     if (j >= n) return;
     const float v[3] = {(float)r[j], (float)g[j], (float)b[j]};
-    const bool init = bk.flags[j] != 0;
+    float* st = px_base<M, 3>(bk, j);
+    uint8_t* fl = px_flag<M, 3>(bk, j);
+    const bool init = *fl != 0;
     Mixture<M, 3> m;
-    load_mix(bk, j, m);
+    load_mix(st, m);
     int t;
-    const uint32_t lab = bank_pixel(m, v, init, k, t);
-    store_mix(bk, j, m);
-    if (!init) bk.flags[j] = 1;
+    const uint32_t lab = bank_pixel(m, st, v, init, k, t);
+    store_mix(st, m);
+    if (!init) *fl = 1;
     if (mask) mask[j] = (uint8_t)lab;
 }
 
@@ -197,13 +221,15 @@ __global__ void __launch_bounds__(kThreads)
     uint32_t lab = 0;
     if (raw != 0) {  // segmenter.cpp:84,128
         const float v[1] = {(float)raw};
-        const bool init = bk.flags[j] != 0;
+        float* st = px_base<M, 1>(bk, j);
+        uint8_t* fl = px_flag<M, 1>(bk, j);
+        const bool init = *fl != 0;
         Mixture<M, 1> m;
-        load_mix(bk, j, m);
+        load_mix(st, m);
         int t;
-        lab = bank_pixel(m, v, init, k, t);
-        store_mix(bk, j, m);
-        if (!init) bk.flags[j] = 1;
+        lab = bank_pixel(m, st, v, init, k, t);
+        store_mix(st, m);
+        if (!init) *fl = 1;
     }
     if (mask) mask[j] = (uint8_t)lab;
 }
@@ -213,13 +239,39 @@ __global__ void k_bank_reset(BankView bk, float sigma0, size_t n) {
     const size_t j = (size_t)blockIdx.x * kThreads + threadIdx.x;
     if (j >= n) return;
     const float var0 = fmul(sigma0, sigma0);
-    const int M = bk.M, C = bk.C;
-    for (int p = 0; p < M * C; ++p) bk.state[(size_t)p * bk.pitch + j] = 0.0f;
+    const int M = bk.M, C = bk.C, NP = bank_planes(M, C);
+    float* s = bk.state + (j / kBlockPx) * bank_stride(M, C) + (j % kBlockPx);
+    for (int p = 0; p < M * C; ++p) s[p * kBlockPx] = 0.0f;
     for (int q = 0; q < M; ++q) {
-        bk.state[(size_t)(M * C + q) * bk.pitch + j] = var0;
-        bk.state[(size_t)(M * C + M + q) * bk.pitch + j] = q == 0 ? 1.0f : 0.0f;
+        s[(M * C + q) * kBlockPx] = var0;
+        s[(M * C + M + q) * kBlockPx] = q == 0 ? 1.0f : 0.0f;
     }
-    bk.flags[j] = 0;
+    reinterpret_cast<uint8_t*>(s - (j % kBlockPx) + NP * kBlockPx)[j % kBlockPx] = 0;
+}
+
+// Flat plane <-> tiled bank (ModelBank::mean_plane / gather / scatter views).
+__global__ void k_bank_gather(BankView bk, int plane, size_t n, void* dst) {
+    const size_t j = (size_t)blockIdx.x * kThreads + threadIdx.x;
+    if (j >= n) return;
+    const int NP = bank_planes(bk.M, bk.C);
+    const float* blk = bk.state + (j / kBlockPx) * bank_stride(bk.M, bk.C);
+    if (plane < 0)
+        static_cast<uint8_t*>(dst)[j] =
+            reinterpret_cast<const uint8_t*>(blk + NP * kBlockPx)[j % kBlockPx];
+    else
+        static_cast<float*>(dst)[j] = blk[plane * kBlockPx + j % kBlockPx];
+}
+
+__global__ void k_bank_scatter(BankView bk, int plane, size_t n, const void* src) {
+    const size_t j = (size_t)blockIdx.x * kThreads + threadIdx.x;
+    if (j >= n) return;
+    const int NP = bank_planes(bk.M, bk.C);
+    float* blk = bk.state + (j / kBlockPx) * bank_stride(bk.M, bk.C);
+    if (plane < 0)
+        reinterpret_cast<uint8_t*>(blk + NP * kBlockPx)[j % kBlockPx] =
+            static_cast<const uint8_t*>(src)[j];
+    else
+        blk[plane * kBlockPx + j % kBlockPx] = static_cast<const float*>(src)[j];
 }
 
 // ---------------------------------------------------------------- K1c fusion
@@ -350,7 +402,7 @@ __global__ void k_render(const __grid_constant__ SceneFrame sc, uint8_t* R, uint
     double base[3] = {__dadd_rn(60.0, __ddiv_rn(__dmul_rn(90.0, (double)x), (double)w)),
                       __dadd_rn(70.0, __ddiv_rn(__dmul_rn(90.0, (double)y), (double)h)),
                       __dadd_rn(80.0, __ddiv_rn(__dmul_rn(80.0, (double)(x + y)), (double)(w + h)))};
-    const uint64_t span = (uint64_t)(2.0 * sc.color_texture + 1.0);
+    const uint64_t span = (uint64_t)__dadd_rn(__dmul_rn(2.0, (double)sc.color_texture), 1.0);
     for (int c = 0; c < 3; ++c) {
         const uint64_t t = hash5(seed, 1, 0, pix, c);
         base[c] = __dadd_rn(base[c], __dsub_rn((double)(t % span), (double)sc.color_texture));
@@ -465,6 +517,14 @@ cudaError_t launch_bank_depth(BankView bk, const MixCfg& k, const uint16_t* d, u
 
 cudaError_t launch_bank_reset(BankView bk, float sigma0, size_t n, cudaStream_t s) {
     return go(k_bank_reset, n, s, bk, sigma0, n);
+}
+
+cudaError_t launch_bank_gather(BankView bk, int plane, size_t n, void* dst, cudaStream_t s) {
+    return go(k_bank_gather, n, s, bk, plane, n, dst);
+}
+
+cudaError_t launch_bank_scatter(BankView bk, int plane, size_t n, const void* src, cudaStream_t s) {
+    return go(k_bank_scatter, n, s, bk, plane, n, src);
 }
 
 cudaError_t launch_fuse(uint8_t* out, int8_t* cpt, const uint8_t* rgb, const uint8_t* dep,

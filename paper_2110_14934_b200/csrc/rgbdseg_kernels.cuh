@@ -10,13 +10,25 @@
 
 namespace rgbdseg_b200 {
 
-// Device layout of one bank: `planes` float planes of `pitch` elements each,
-// plane order = ModelBank (segmenter.hpp:51-54): mean(i,c) = i*C + c,
-// variance(i) = M*C + i, weight(i) = M*C + M + i.  Flags: one uint8 plane.
+// Device layout of one bank: TILED structure-of-arrays.  Pixels are grouped
+// in blocks of 32 (one warp); block b stores, for its 32 pixels, float plane
+// 0..NP-1 of ModelBank's plane order (segmenter.hpp:51-54: mean(i,c) = i*C+c,
+// variance(i) = M*C+i, weight(i) = M*C+M+i) as 32 consecutive floats each,
+// then one 128-byte slot whose first 32 bytes are the initialised flags.
+// A warp's access to one plane is still one full 128-byte line (SoA
+// coalescing), but every plane of a pixel sits at an
+// immediate offset p*128 from one per-thread address, so the kernels issue
+// no per-plane 64-bit address arithmetic.  bank_download/upload gather and
+// scatter the reference's flat planes.
+constexpr int kBlockPx = 32;
+
+__host__ __device__ constexpr int bank_planes(int M, int C) { return M * C + 2 * M; }
+__host__ __device__ constexpr int bank_stride(int M, int C) {  // floats per block
+    return (bank_planes(M, C) + 1) * kBlockPx;
+}
+
 struct BankView {
-    float* state;
-    uint8_t* flags;
-    size_t pitch;
+    float* state;  // nblocks * bank_stride(M, C) floats
     int M;
     int C;
 };
@@ -55,6 +67,9 @@ cudaError_t launch_bank_color(BankView bank, const MixCfg& k, const uint8_t* r, 
 cudaError_t launch_bank_depth(BankView bank, const MixCfg& k, const uint16_t* d, uint8_t* mask,
                               size_t n, cudaStream_t s);
 cudaError_t launch_bank_reset(BankView bank, float sigma0, size_t n, cudaStream_t s);
+// plane = ModelBank plane id, or -1 for the flags (uint8).  dst/src: npx elements.
+cudaError_t launch_bank_gather(BankView bank, int plane, size_t n, void* dst, cudaStream_t s);
+cudaError_t launch_bank_scatter(BankView bank, int plane, size_t n, const void* src, cudaStream_t s);
 cudaError_t launch_fuse(uint8_t* out, int8_t* cpt, const uint8_t* rgb, const uint8_t* dep,
                         uint8_t* out_copy, int limit, size_t n, cudaStream_t s);
 

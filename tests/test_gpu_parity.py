@@ -399,3 +399,22 @@ def test_processor_tail_and_misaligned_inputs(R, port, cuda, variant):
     P = proc.depth_bank().planes().reshape(-1, S, w * h)
     for s in range(S):
         assert P[:, s].tobytes() == orc[s].depth.planes().tobytes()
+
+
+def test_fast_sqrt_div_match_ieee_intrinsics(cuda, tmp_path):
+    """The branch-free fast sqrt / div of gmm_step_fast against __fsqrt_rn /
+    __fdiv_rn wherever they report ok: all 2^32 sqrt inputs, all 2^32
+    numerators for six divisors, and 2^34 random pairs."""
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = tmp_path / "fmc"
+    subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17",
+                    "-fmad=false", "-prec-div=true", "-prec-sqrt=true", "-ftz=false", "-o",
+                    str(exe), os.path.join(root, "tests", "native", "fast_math_check.cu")],
+                   check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    counts = dict(zip(r.stdout.split()[0::2], map(int, r.stdout.split()[1::2])))
+    assert counts["sqrt_ok"] > 2_000_000_000 and counts["div_all_ok"] > 10_000_000_000
