@@ -10,6 +10,7 @@
 using namespace rgbdseg_b200;
 
 __device__ unsigned long long g_cnt[8];
+__device__ unsigned int g_bad[16][4];  // first failing cases: a, b, fast, ieee
 
 __device__ __forceinline__ uint64_t mix(uint64_t z) {
     z += 0x9e3779b97f4a7c15ULL;
@@ -72,7 +73,17 @@ __global__ void div_random(uint64_t seed, int per_thread) {
         const float q = fdiv_fast(a, b, ok);
         if (ok) {
             ++ok_n;
-            if (!same(q, __fdiv_rn(a, b))) ++bad;
+            const float ref = __fdiv_rn(a, b);
+            if (!same(q, ref)) {
+                ++bad;
+                const unsigned slot = atomicAdd((unsigned*)&g_cnt[6], 1u);
+                if (slot < 16) {
+                    g_bad[slot][0] = __float_as_uint(a);
+                    g_bad[slot][1] = __float_as_uint(b);
+                    g_bad[slot][2] = __float_as_uint(q);
+                    g_bad[slot][3] = __float_as_uint(ref);
+                }
+            }
         }
     }
     atomicAdd(&g_cnt[4], ok_n);
@@ -86,11 +97,17 @@ int main() {
     const float divisors[] = {3.0f, 1.0f, 0.99999994f, 1.0000001f, 1.7f, 0.05f};
     for (float b : divisors) div_all_a<<<(1u << 28) / 256, 256>>>(b);
     div_random<<<148 * 64, 256>>>(12345, 1 << 12);
+    div_random<<<148 * 64, 256>>>(777, 1 << 12);
     if (cudaDeviceSynchronize() != cudaSuccess) {
         printf("CUDA error\n");
         return 2;
     }
     cudaMemcpyFromSymbol(h, g_cnt, sizeof h);
+    unsigned int bad[16][4];
+    cudaMemcpyFromSymbol(bad, g_bad, sizeof bad);
+    for (unsigned i = 0; i < 16 && i < (unsigned)h[6]; ++i)
+        fprintf(stderr, "bad a=%08x b=%08x fast=%08x ieee=%08x\n", bad[i][0], bad[i][1], bad[i][2],
+                bad[i][3]);
     printf("sqrt_ok %llu sqrt_bad %llu div_all_ok %llu div_all_bad %llu div_rand_ok %llu "
            "div_rand_bad %llu\n",
            h[0], h[1], h[2], h[3], h[4], h[5]);
