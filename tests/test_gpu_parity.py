@@ -417,4 +417,5 @@ def test_fast_sqrt_div_match_ieee_intrinsics(cuda, tmp_path):
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     counts = dict(zip(r.stdout.split()[0::2], map(int, r.stdout.split()[1::2])))
-    assert counts["sqrt_ok"] > 2_000_000_000 and counts["div_all_ok"] > 10_000_000_000
+    # the sqrt fast range is bits 0x0d000000..0x7f7fffff (1.92e9 inputs)
+    assert counts["sqrt_ok"] > 1_900_000_000 and counts["div_all_ok"] > 10_000_000_000
