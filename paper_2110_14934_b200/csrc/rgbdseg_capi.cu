@@ -74,8 +74,10 @@ int validate_cfg(const rgbdseg_mixture_cfg* c) {
 }
 
 MixCfg to_k(const rgbdseg_mixture_cfg& c) {
+    // gmm_step_fast divides by max(w, alpha): alpha must sit in its exact range
+    const int fast = c.learning_rate >= 0x1p-60f && c.learning_rate < 0x1p61f;
     return MixCfg{c.learning_rate,  c.match_lambda,   c.background_threshold,
-                  c.initial_sigma, c.initial_weight, c.variance_floor};
+                  c.initial_sigma, c.initial_weight, c.variance_floor, fast};
 }
 
 bool on_device(const void* p) {

@@ -113,7 +113,7 @@ __device__ __forceinline__ uint32_t bank_pixel(Mixture<M, C>& m, const float* sr
         touched = -1;
         return 0u;
     }
-    bool ok = true;
+    bool ok = k.fast != 0;
     uint32_t label = gmm_step_fast(m, v, k, touched, ok);
     if (!ok) {
         load_mix(src, m);

@@ -28,7 +28,7 @@ static int step_t(Rec* r, const float* v, const Cfg* k) {
     }
     float vv[C];
     for (int c = 0; c < C; ++c) vv[c] = v[c];
-    const MixCfg kk{k->alpha, k->lambda, k->T, k->sigma0, k->w_new, k->var_floor};
+    const MixCfg kk{k->alpha, k->lambda, k->T, k->sigma0, k->w_new, k->var_floor, 0};
     const int lab = (int)gmm_step(m, vv, kk);
     for (int i = 0; i < M; ++i) {
         for (int c = 0; c < C; ++c) r->means[i * C + c] = m.mu[i][c];

@@ -419,3 +419,45 @@ def test_fast_sqrt_div_match_ieee_intrinsics(cuda, tmp_path):
     counts = dict(zip(r.stdout.split()[0::2], map(int, r.stdout.split()[1::2])))
     # the sqrt fast range is bits 0x0d000000..0x7f7fffff (1.92e9 inputs)
     assert counts["sqrt_ok"] > 1_900_000_000 and counts["div_all_ok"] > 10_000_000_000
+
+
+@pytest.mark.parametrize("alpha", [0.05, 1e-20])
+@pytest.mark.parametrize("mode", ["Color3", "Depth1"])
+def test_bank_extreme_states_take_the_exact_replay(R, port, mode, alpha):
+    """States outside the fast step's ranges (weights below 2^-60 or
+    denormal, -0 or NaN weights, variances above 2^113 or below 2^-100, and
+    alpha below 2^-60 disabling the fast step) are replayed by the generic
+    step: masks and every bank word equal the oracle (NaN-aware)."""
+    rng = np.random.default_rng(17)
+    w, h, M = 41, 29, 5
+    Ch = 3 if mode == "Color3" else 1
+    oc = (O.color_cfg if Ch == 3 else O.depth_cfg)(M, learning_rate=alpha)
+    cfg = rcfg(R, oc)
+    n = w * h
+    planes = np.zeros((M * Ch + 2 * M, n), np.float32)
+    planes[: M * Ch] = rng.uniform(0, 255 if Ch == 3 else 4000, (M * Ch, n))
+    var = rng.choice(np.array([4.0, 30.0, 225.0, 1e35, 1e-31, 3e-38], np.float32), (M, n),
+                     p=[0.4, 0.3, 0.2, 0.04, 0.03, 0.03])
+    wts = rng.choice(np.array([0.0, 0.2, 0.5, 1e-25, 1e-40, -0.0, np.nan], np.float32), (M, n),
+                     p=[0.3, 0.3, 0.3, 0.04, 0.03, 0.02, 0.01])
+    planes[M * Ch: M * Ch + M] = var
+    planes[M * Ch + M:] = wts
+    bank = R.ModelBank(w, h, mode, cfg)
+    for p in range(planes.shape[0]):
+        bank.upload_plane(p, planes[p].reshape(h, w))
+    bank.upload_plane(-1, np.ones((h, w), np.uint8))
+    ob = O.PortBank(port, n, Ch, oc)
+    ob.state[:] = planes.reshape(-1)
+    ob.flags[:] = 1
+    for f in range(6):
+        if Ch == 3:
+            r, g, b = (rng.integers(0, 256, (h, w), dtype=np.uint8) for _ in range(3))
+            m = R.segment_color(bank, r, g, b, cfg)
+            mo = ob.segment_color(r, g, b)
+        else:
+            d = rng.integers(1, 5000, (h, w)).astype(np.uint16)
+            m = R.segment_depth(bank, d, cfg)
+            mo = ob.segment_depth(d)
+        assert np.array_equal(m.ravel(), mo), f
+        got = bank.planes()
+        assert np.array_equal(got, ob.planes(), equal_nan=True), f
