@@ -461,3 +461,20 @@ def test_bank_extreme_states_take_the_exact_replay(R, port, mode, alpha):
         assert np.array_equal(m.ravel(), mo), f
         got = bank.planes()
         assert np.array_equal(got, ob.planes(), equal_nan=True), f
+
+
+def test_cpp_dropin_matches_reference_sequence_processor(cuda):
+    """integration/dropin_test: the reference's own SequenceProcessor (CPU)
+    and rgbdseg::b200::SequenceProcessor (this library) on the same
+    render_frame sequence -> identical FrameMasks and ModelBanks."""
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "integration", "_build", "dropin_test")
+    if not os.path.exists(exe):
+        pytest.skip("integration/_build/dropin_test not built (needs /root/reference)")
+    for args in (["40", "320", "240", "5"], ["12", "640", "480", "3"]):
+        r = subprocess.run([exe, *args], capture_output=True, text=True, timeout=600)
+        print(r.stdout)
+        assert r.returncode == 0, r.stdout + r.stderr
+        assert "banks identical" in r.stdout
