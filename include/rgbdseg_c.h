@@ -134,6 +134,32 @@ int rgbdseg_fusion_step(rgbdseg_fusion* fs, const uint8_t* rgb_mask, const uint8
 int rgbdseg_fusion_download(const rgbdseg_fusion* fs, uint8_t* out, int8_t* cpt);
 int rgbdseg_fusion_upload(rgbdseg_fusion* fs, const uint8_t* out, const int8_t* cpt);
 
+/* ---- CameraRig / register_mask / dilate_mask: registration.hpp:10-38 -----
+ * Depth->colour registration for unregistered sequences (processor.cpp:175-179):
+ * back-project each valid foreground depth pixel, apply (R, t), project with
+ * lround into the colour grid, splat, then a square dilation of radius r.
+ * Same fp64 arithmetic as the reference, bit-identical masks. */
+typedef struct rgbdseg_camera_rig {
+    double depth_fx, depth_fy, depth_cx, depth_cy; /* Pinhole depth_cam */
+    double color_fx, color_fy, color_cx, color_cy; /* Pinhole color_cam */
+    double rotation[9];                            /* row-major */
+    double translation_mm[3];
+    double depth_scale;                            /* mm per raw depth unit */
+} rgbdseg_camera_rig;
+
+/* CameraRig::identity(fx, fy, cx, cy), registration.cpp:28-33 */
+void rgbdseg_camera_rig_identity(rgbdseg_camera_rig* rig, double fx, double fy, double cx,
+                                 double cy);
+/* CameraRig::validate, registration.cpp:10-26 (same messages) */
+int rgbdseg_camera_rig_validate(const rgbdseg_camera_rig* rig);
+/* register_mask(mask, depth, rig, cw, ch, radius), registration.cpp:50-78.
+ * mask/depth: dw*dh (host or device); out: cw*ch.  Synchronous. */
+int rgbdseg_register_mask(const uint8_t* depth_mask, const uint16_t* depth_raw, int dw, int dh,
+                          const rgbdseg_camera_rig* rig, int cw, int ch, int dilation_radius,
+                          uint8_t* out, int device);
+/* dilate_mask(mask, radius), registration.cpp:33-48.  Synchronous. */
+int rgbdseg_dilate_mask(const uint8_t* mask, int w, int h, int radius, uint8_t* out, int device);
+
 /* ---- SequenceProcessor: processor.hpp:60-80, process = processor.cpp:158-184
  * Fused method on a registered sequence: colour bank + depth bank + List-1
  * fusion, executed as ONE kernel per frame batch over `streams` independent
@@ -148,6 +174,9 @@ typedef struct rgbdseg_processor_cfg {
     int fusion_initial_label; /* 0 or 1 */
     int device;
     int host_chunks;       /* 0 = auto: H2D/compute/D2H overlap chunks for host frames */
+    int registered;        /* 1 (default): depth already in the colour grid */
+    rgbdseg_camera_rig rig; /* used when registered == 0 (must validate) */
+    int dilation_radius;   /* >= 0, default 1 (processor.hpp:26) */
 } rgbdseg_processor_cfg;
 
 void rgbdseg_processor_defaults(rgbdseg_processor_cfg* cfg, int width, int height);

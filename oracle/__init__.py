@@ -197,11 +197,21 @@ class PortBank:
         return mask
 
 
+def rig_array(depth_cam, color_cam, rotation, translation, scale) -> np.ndarray:
+    """Pack a CameraRig as the 21 doubles orc_register / rref_register_mask take."""
+    return np.ascontiguousarray(list(depth_cam) + list(color_cam) + list(rotation) +
+                                list(translation) + [scale], np.float64)
+
+
 class PortProcessor:
     """Colour bank + depth bank + List-1 fusion, the order of
-    SequenceProcessor::process (processor.cpp:158-184), registered sequence."""
+    SequenceProcessor::process (processor.cpp:158-184).  With `rig` (21
+    doubles) and width/height the sequence is unregistered: the depth mask is
+    registered and dilated (processor.cpp:175-179) before fusion."""
 
-    def __init__(self, port: Port, npx: int, ccfg: Cfg, dcfg: Cfg, limit=3, initial_label=0):
+    def __init__(self, port: Port, npx: int, ccfg: Cfg, dcfg: Cfg, limit=3, initial_label=0,
+                 rig=None, width=0, height=0, radius=1):
+        self.rig, self.w, self.h, self.radius = rig, width, height, radius
         self.port = port
         self.color = PortBank(port, npx, 3, ccfg)
         self.depth = PortBank(port, npx, 1, dcfg)
@@ -213,7 +223,14 @@ class PortProcessor:
     def process(self, r, g, b, d):
         rgb = self.color.segment_color(r, g, b)
         dep = self.depth.segment_depth(d)
-        self.port.lib.orc_fuse(self.out, self.cpt, self.out.size, self.limit, rgb, dep)
+        reg = dep
+        if self.rig is not None:
+            n = self.w * self.h
+            reg = np.empty(n, np.uint8)
+            scratch = np.empty(n, np.uint8)
+            self.port.lib.orc_register(dep, np.ascontiguousarray(d).ravel(), self.w, self.h,
+                                       self.rig, self.w, self.h, self.radius, scratch, reg)
+        self.port.lib.orc_fuse(self.out, self.cpt, self.out.size, self.limit, rgb, reg)
         return rgb, dep, self.out.copy()
 
 
@@ -254,6 +271,9 @@ class Ref:
         L.rref_processor_create.argtypes = [C.c_int, C.c_int, C.POINTER(Cfg), C.POINTER(Cfg),
                                             C.c_int, C.c_int, C.c_int]
         L.rref_processor_destroy.argtypes = [C.c_void_p]
+        L.rref_processor_create_rig.restype = C.c_void_p
+        L.rref_processor_create_rig.argtypes = [C.c_int, C.c_int, C.POINTER(Cfg), C.POINTER(Cfg),
+                                                C.c_int, C.c_int, C.c_int, _f64p, C.c_int]
         L.rref_processor_process.argtypes = [C.c_void_p, _u8p, _u8p, _u8p, _u16p, C.c_void_p,
                                              C.c_void_p, C.c_void_p]
         L.rref_processor_bank_get.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
@@ -304,11 +324,16 @@ class RefProcessor:
     """The reference SequenceProcessor (fused, registered, SoA)."""
 
     def __init__(self, ref: Ref, width, height, ccfg: Cfg, dcfg: Cfg, limit=3, initial_label=0,
-                 workers=1):
+                 workers=1, rig=None, radius=1):
         self.ref, self.w, self.h = ref, width, height
         self.ccfg, self.dcfg = ccfg, dcfg
-        self.p = ref.lib.rref_processor_create(width, height, C.byref(ccfg), C.byref(dcfg), limit,
-                                               initial_label, workers)
+        if rig is None:
+            self.p = ref.lib.rref_processor_create(width, height, C.byref(ccfg), C.byref(dcfg),
+                                                   limit, initial_label, workers)
+        else:
+            self.p = ref.lib.rref_processor_create_rig(width, height, C.byref(ccfg),
+                                                       C.byref(dcfg), limit, initial_label,
+                                                       workers, rig, radius)
         if not self.p:
             raise ValueError(ref.lib.rref_last_error().decode())
 

@@ -315,6 +315,34 @@ void* rref_processor_create(int w, int h, const RefCfg* color, const RefCfg* dep
         return nullptr;
     }
 }
+// Unregistered sequence: depth masks go through register_mask (+dilation)
+// before fusion (processor.cpp:175-179).  rig packed as in rref_register_mask.
+void* rref_processor_create_rig(int w, int h, const RefCfg* color, const RefCfg* depth, int limit,
+                                int initial_label, int workers, const double* rig, int radius) {
+    try {
+        RunConfig cfg = RunConfig::defaults();
+        cfg.color_gmm = to_ref(color);
+        cfg.depth_gmm = to_ref(depth);
+        cfg.fusion_counter_limit = limit;
+        cfg.fusion_initial_label = static_cast<uint8_t>(initial_label);
+        cfg.workers = workers;
+        cfg.pipeline = false;
+        cfg.dilation_radius = radius;
+        CameraRig r;
+        r.depth_cam = {rig[0], rig[1], rig[2], rig[3]};
+        r.color_cam = {rig[4], rig[5], rig[6], rig[7]};
+        for (int i = 0; i < 9; ++i) r.rotation[i] = rig[8 + i];
+        for (int i = 0; i < 3; ++i) r.translation_mm[i] = rig[17 + i];
+        r.depth_scale = rig[20];
+        MethodSet ms;
+        ms.fused = true;
+        return new Proc{w, h, std::make_unique<SequenceProcessor>(w, h, ms, cfg, r, false)};
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+
 void rref_processor_destroy(void* p) { delete static_cast<Proc*>(p); }
 
 // Any of rgb_mask / depth_mask / fused may be null.

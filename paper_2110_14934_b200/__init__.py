@@ -6,6 +6,7 @@ from ._lib import launch_count  # noqa: F401  (fails loudly without the CUDA lib
 from .rgbdseg import (  # noqa: F401
     PIXEL_MIXTURE_DTYPE,
     BankMode,
+    CameraRig,
     FrameMasks,
     FusionState,
     MixtureConfig,
@@ -15,9 +16,11 @@ from .rgbdseg import (  # noqa: F401
     SequenceProcessor,
     builtin_scenario_names,
     default_config_json,
+    dilate_mask,
     fuse_step,
     init_mixture,
     init_mixtures,
+    register_mask,
     render_scenario,
     reset_state,
     segment_color,

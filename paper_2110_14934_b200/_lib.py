@@ -40,6 +40,20 @@ class PixelMixtureRec(C.Structure):
     ]
 
 
+class CameraRigC(C.Structure):
+    """rgbdseg_camera_rig = CameraRig (registration.hpp:16-26)."""
+
+    _fields_ = [
+        ("depth_fx", C.c_double), ("depth_fy", C.c_double),
+        ("depth_cx", C.c_double), ("depth_cy", C.c_double),
+        ("color_fx", C.c_double), ("color_fy", C.c_double),
+        ("color_cx", C.c_double), ("color_cy", C.c_double),
+        ("rotation", C.c_double * 9),
+        ("translation_mm", C.c_double * 3),
+        ("depth_scale", C.c_double),
+    ]
+
+
 class ProcessorCfg(C.Structure):
     _fields_ = [
         ("width", C.c_int),
@@ -51,6 +65,9 @@ class ProcessorCfg(C.Structure):
         ("fusion_initial_label", C.c_int),
         ("device", C.c_int),
         ("host_chunks", C.c_int),
+        ("registered", C.c_int),
+        ("rig", CameraRigC),
+        ("dilation_radius", C.c_int),
     ]
 
 
@@ -77,6 +94,11 @@ SIGNATURES = {
     "rgbdseg_fusion_step": (_i, [_vp, _vp, _vp, _vp]),
     "rgbdseg_fusion_download": (_i, [_vp, _vp, _vp]),
     "rgbdseg_fusion_upload": (_i, [_vp, _vp, _vp]),
+    "rgbdseg_camera_rig_identity": (None, [C.POINTER(CameraRigC), C.c_double, C.c_double,
+                                            C.c_double, C.c_double]),
+    "rgbdseg_camera_rig_validate": (_i, [C.POINTER(CameraRigC)]),
+    "rgbdseg_register_mask": (_i, [_vp, _vp, _i, _i, C.POINTER(CameraRigC), _i, _i, _i, _vp, _i]),
+    "rgbdseg_dilate_mask": (_i, [_vp, _i, _i, _i, _vp, _i]),
     "rgbdseg_processor_defaults": (None, [C.POINTER(ProcessorCfg), _i, _i]),
     "rgbdseg_processor_create": (_i, [C.POINTER(ProcessorCfg), C.POINTER(_vp)]),
     "rgbdseg_processor_destroy": (None, [_vp]),

@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -193,6 +194,9 @@ struct rgbdseg_processor {
     uint64_t seq = 0;
     int64_t frames = 0;
     int variant = kAuto;
+    // unregistered sequences: whole-frame scratch (inputs, masks, splat)
+    Scratch u_in, u_masks;
+    cudaEvent_t u_h2d = nullptr, u_k = nullptr;
 };
 
 extern "C" {
@@ -502,6 +506,92 @@ int rgbdseg_fusion_upload(rgbdseg_fusion* f, const uint8_t* out, const int8_t* c
     return RGBDSEG_OK;
 }
 
+// ------------------------------------------------------------ registration
+void rgbdseg_camera_rig_identity(rgbdseg_camera_rig* r, double fx, double fy, double cx,
+                                 double cy) {
+    std::memset(r, 0, sizeof *r);
+    r->depth_fx = r->color_fx = fx;
+    r->depth_fy = r->color_fy = fy;
+    r->depth_cx = r->color_cx = cx;
+    r->depth_cy = r->color_cy = cy;
+    r->rotation[0] = r->rotation[4] = r->rotation[8] = 1.0;
+    r->depth_scale = 1.0;
+}
+
+int rgbdseg_camera_rig_validate(const rgbdseg_camera_rig* r) {
+    if (!r) return fail(RGBDSEG_EINVAL, "CameraRig: null");
+    if (!(r->depth_fx > 0.0 && r->depth_fy > 0.0 && r->color_fx > 0.0 && r->color_fy > 0.0))
+        return fail(RGBDSEG_EINVAL, "CameraRig: focal lengths must be positive");
+    if (!(r->depth_scale > 0.0)) return fail(RGBDSEG_EINVAL, "CameraRig: depth_scale must be positive");
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {  // R^T R == I within 1e-9
+            double dot = 0.0;
+            for (int k = 0; k < 3; ++k) dot += r->rotation[k * 3 + i] * r->rotation[k * 3 + j];
+            if (std::fabs(dot - (i == j ? 1.0 : 0.0)) > 1e-9)
+                return fail(RGBDSEG_EINVAL, "CameraRig: rotation is not orthonormal");
+        }
+    return RGBDSEG_OK;
+}
+
+static RigDev to_dev(const rgbdseg_camera_rig& r) {
+    RigDev d;
+    d.dfx = r.depth_fx;
+    d.dfy = r.depth_fy;
+    d.dcx = r.depth_cx;
+    d.dcy = r.depth_cy;
+    d.cfx = r.color_fx;
+    d.cfy = r.color_fy;
+    d.ccx = r.color_cx;
+    d.ccy = r.color_cy;
+    for (int i = 0; i < 9; ++i) d.R[i] = r.rotation[i];
+    for (int i = 0; i < 3; ++i) d.t[i] = r.translation_mm[i];
+    d.scale = r.depth_scale;
+    return d;
+}
+
+int rgbdseg_dilate_mask(const uint8_t* mask, int w, int h, int radius, uint8_t* out, int device) {
+    if (int rc = check_dims(w, h, 1)) return rc;
+    GUARD(device);
+    const size_t n = (size_t)w * h;
+    Scratch sin, sbuf;
+    const void* din;
+    if (int rc = stage_in(mask, n, sin, &din, 0)) return rc;
+    void* buf;
+    if (int rc = sbuf.get(2 * n, &buf)) return rc;
+    uint8_t* tmp = static_cast<uint8_t*>(buf);
+    uint8_t* res = on_device(out) ? out : tmp + n;
+    CU(launch_dilate((const uint8_t*)din, tmp, res, w, h, 1, radius, 0));
+    if (res != out) CU(cudaMemcpyAsync(out, res, n, cudaMemcpyDefault, 0));
+    CU(cudaStreamSynchronize(0));
+    return RGBDSEG_OK;
+}
+
+int rgbdseg_register_mask(const uint8_t* mask, const uint16_t* depth, int dw, int dh,
+                          const rgbdseg_camera_rig* rig, int cw, int ch, int radius, uint8_t* out,
+                          int device) {
+    if (int rc = check_dims(dw, dh, 1)) return rc;
+    if (int rc = check_dims(cw, ch, 1)) return rc;
+    if (int rc = rgbdseg_camera_rig_validate(rig)) return rc;  // registration.cpp:57
+    GUARD(device);
+    const size_t nd = (size_t)dw * dh, nc = (size_t)cw * ch;
+    Scratch sm, sd, sbuf;
+    const void *dm, *dd;
+    if (int rc = stage_in(mask, nd, sm, &dm, 0)) return rc;
+    if (int rc = stage_in(depth, 2 * nd, sd, &dd, 0)) return rc;
+    void* buf;
+    if (int rc = sbuf.get(3 * nc, &buf)) return rc;
+    uint8_t* splat = static_cast<uint8_t*>(buf);
+    uint8_t* tmp = splat + nc;
+    uint8_t* res = on_device(out) ? out : splat + 2 * nc;
+    CU(cudaMemsetAsync(splat, 0, nc, 0));
+    CU(launch_register_splat((const uint8_t*)dm, (const uint16_t*)dd, dw, dh, 1, to_dev(*rig), cw,
+                             ch, splat, 0));
+    CU(launch_dilate(splat, tmp, res, cw, ch, 1, radius, 0));
+    if (res != out) CU(cudaMemcpyAsync(out, res, nc, cudaMemcpyDefault, 0));
+    CU(cudaStreamSynchronize(0));
+    return RGBDSEG_OK;
+}
+
 // ------------------------------------------------------------ processor
 void rgbdseg_processor_defaults(rgbdseg_processor_cfg* c, int width, int height) {
     std::memset(c, 0, sizeof *c);
@@ -516,6 +606,9 @@ void rgbdseg_processor_defaults(rgbdseg_processor_cfg* c, int width, int height)
     c->fusion_initial_label = 0;
     c->device = 0;
     c->host_chunks = 0;
+    c->registered = 1;
+    rgbdseg_camera_rig_identity(&c->rig, 525.0, 525.0, 319.5, 239.5);
+    c->dilation_radius = 1;
 }
 
 void rgbdseg_processor_destroy(rgbdseg_processor* p) {
@@ -535,6 +628,8 @@ void rgbdseg_processor_destroy(rgbdseg_processor* p) {
     }
     for (cudaEvent_t ev : p->chunk_d2h)
         if (ev) cudaEventDestroy(ev);
+    for (cudaEvent_t ev : {p->u_h2d, p->u_k})
+        if (ev) cudaEventDestroy(ev);
     for (cudaStream_t s : {p->sc, p->sh2d, p->sd2h})
         if (s) cudaStreamDestroy(s);
     rgbdseg_bank_destroy(p->color);
@@ -553,6 +648,11 @@ int rgbdseg_processor_create(const rgbdseg_processor_cfg* cfg, rgbdseg_processor
         return fail(RGBDSEG_EINVAL, "config: fusion counter_limit must be >= 1");
     if (cfg->fusion_initial_label < 0 || cfg->fusion_initial_label > 1)
         return fail(RGBDSEG_EINVAL, "config: fusion initial_label must be 0 or 1");
+    if (cfg->dilation_radius < 0)
+        return fail(RGBDSEG_EINVAL, "config: dilation_radius must be >= 0");
+    if (!cfg->registered) {  // processor.cpp:131-132, registration.cpp:57
+        if (int rc = rgbdseg_camera_rig_validate(&cfg->rig)) return rc;
+    }
     GUARD(cfg->device);
     auto* p = new rgbdseg_processor();
     p->cfg = *cfg;
@@ -582,6 +682,8 @@ int rgbdseg_processor_create(const rgbdseg_processor_cfg* cfg, rgbdseg_processor
         p->chunk_d2h.assign(chunks, nullptr);
         for (auto& ev : p->chunk_d2h)
             if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+        for (cudaEvent_t* ev : {&p->u_h2d, &p->u_k})
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
         if (e != cudaSuccess) rc = cuda_fail(e, "processor_create");
     }
     if (rc) {
@@ -613,7 +715,71 @@ static FusedArgs base_args(const rgbdseg_processor* p) {
     a.ck = to_k(p->cfg.color);
     a.dk = to_k(p->cfg.depth);
     a.limit = p->cfg.fusion_counter_limit;
+    a.fuse = 1;
     return a;
+}
+
+// Unregistered sequence (processor.cpp:175-179): both banks step and write
+// their masks, the depth mask is registered into the colour grid and
+// dilated, then List 1 fuses -- whole frames, in stream order.
+static int submit_unregistered(rgbdseg_processor* p, const uint8_t* r, const uint8_t* g,
+                               const uint8_t* b, const uint16_t* depth, uint8_t* fused_out,
+                               uint8_t* rgb_out, uint8_t* depth_out) {
+    const size_t n = p->npx;
+    const int w = p->cfg.width, h = p->cfg.height, S = p->cfg.streams;
+    void* ibuf;
+    if (int rc = p->u_in.get(5 * n, &ibuf)) return rc;
+    void* mbuf;
+    if (int rc = p->u_masks.get(5 * n, &mbuf)) return rc;
+    uint8_t* in = static_cast<uint8_t*>(ibuf);
+    uint8_t *rgbm = static_cast<uint8_t*>(mbuf), *depm = rgbm + n, *splat = depm + n,
+            *tmp = splat + n, *reg = tmp + n;
+    // the previous frame's D2H must have drained the mask scratch
+    CU(cudaStreamWaitEvent(p->sh2d, p->u_k, 0));
+    const uint8_t* src[4] = {r, g, b, reinterpret_cast<const uint8_t*>(depth)};
+    const uint8_t* dev[4];
+    size_t off = 0;
+    for (int k = 0; k < 4; ++k) {
+        const size_t bytes = k == 3 ? 2 * n : n;
+        if (on_device(src[k])) {
+            dev[k] = src[k];
+        } else {
+            CU(cudaMemcpyAsync(in + off, src[k], bytes, cudaMemcpyDefault, p->sh2d));
+            dev[k] = in + off;
+        }
+        off += bytes;
+    }
+    CU(cudaEventRecord(p->u_h2d, p->sh2d));
+    CU(cudaStreamWaitEvent(p->sc, p->u_h2d, 0));
+    for (cudaEvent_t ev : p->chunk_d2h) CU(cudaStreamWaitEvent(p->sc, ev, 0));
+    FusedArgs a = base_args(p);
+    a.fuse = 0;
+    a.r = dev[0];
+    a.g = dev[1];
+    a.b = dev[2];
+    a.d = reinterpret_cast<const uint16_t*>(dev[3]);
+    a.rgb_mask = rgbm;
+    a.depth_mask = depm;
+    a.out = p->fusion->out;
+    a.cpt = p->fusion->cpt;
+    a.base = 0;
+    a.n = n;
+    CU(launch_fused(a, p->variant, p->sc));
+    CU(cudaMemsetAsync(splat, 0, n, p->sc));
+    CU(launch_register_splat(depm, a.d, w, h, S, to_dev(p->cfg.rig), w, h, splat, p->sc));
+    CU(launch_dilate(splat, tmp, reg, w, h, S, p->cfg.dilation_radius, p->sc));
+    uint8_t* fcopy = (fused_out && on_device(fused_out)) ? fused_out : nullptr;
+    CU(launch_fuse(p->fusion->out, p->fusion->cpt, rgbm, reg, fcopy, p->cfg.fusion_counter_limit,
+                   n, p->sc));
+    CU(cudaEventRecord(p->u_k, p->sc));
+    CU(cudaStreamWaitEvent(p->sd2h, p->u_k, 0));
+    if (fused_out && !fcopy) CU(cudaMemcpyAsync(fused_out, p->fusion->out, n, cudaMemcpyDefault, p->sd2h));
+    if (rgb_out) CU(cudaMemcpyAsync(rgb_out, rgbm, n, cudaMemcpyDefault, p->sd2h));
+    if (depth_out) CU(cudaMemcpyAsync(depth_out, depm, n, cudaMemcpyDefault, p->sd2h));
+    CU(cudaEventRecord(p->u_k, p->sd2h));
+    if (!p->chunk_d2h.empty()) CU(cudaEventRecord(p->chunk_d2h[0], p->sd2h));
+    ++p->frames;
+    return RGBDSEG_OK;
 }
 
 int rgbdseg_processor_submit(rgbdseg_processor* p, const uint8_t* r, const uint8_t* g,
@@ -621,6 +787,8 @@ int rgbdseg_processor_submit(rgbdseg_processor* p, const uint8_t* r, const uint8
                              uint8_t* rgb_out, uint8_t* depth_out) {
     if (!r || !g || !b || !depth) return fail(RGBDSEG_EINVAL, "process: null input plane");
     GUARD(p->cfg.device);
+    if (!p->cfg.registered)
+        return submit_unregistered(p, r, g, b, depth, fused_out, rgb_out, depth_out);
     const bool dr = on_device(r), dg = on_device(g), db = on_device(b), dd = on_device(depth);
     const bool dfo = on_device(fused_out), dro = on_device(rgb_out), ddo = on_device(depth_out);
     const bool all_device = dr && dg && db && dd && (!fused_out || dfo) && (!rgb_out || dro) &&

@@ -144,8 +144,8 @@ __global__ void __launch_bounds__(kThreads, RGBDSEG_FUSED_MIN_BLOCKS)
     uint8_t* dfl = px_flag<MD, 1>(a.depth, j);
     const bool cinit = ld_stream(cfl) != 0;
     const bool dinit = ld_stream(dfl) != 0;
-    const uint32_t out0 = ld_stream(a.out + i);
-    const int cpt0 = (int)ld_stream(a.cpt + i);
+    const uint32_t out0 = a.fuse ? ld_stream(a.out + i) : 0u;
+    const int cpt0 = a.fuse ? (int)ld_stream(a.cpt + i) : 0;
     Mixture<MC, 3> cm;
     Mixture<MD, 1> dm;
     load_mix(cs, cm);
@@ -182,9 +182,11 @@ __global__ void __launch_bounds__(kThreads, RGBDSEG_FUSED_MIN_BLOCKS)
     // ---- List-1 fusion on the registered depth mask ----
     uint32_t out = out0;
     int cpt = cpt0;
-    fuse_pixel(lc, ld, a.limit, out, cpt);
-    if (!kElide || out != out0) st_stream(a.out + i, (uint8_t)out);
-    if (!kElide || cpt != cpt0) st_stream(a.cpt + i, (int8_t)cpt);
+    if (a.fuse) {
+        fuse_pixel(lc, ld, a.limit, out, cpt);
+        if (!kElide || out != out0) st_stream(a.out + i, (uint8_t)out);
+        if (!kElide || cpt != cpt0) st_stream(a.cpt + i, (int8_t)cpt);
+    }
     if (a.rgb_mask) st_stream(a.rgb_mask + i, (uint8_t)lc);
     if (a.depth_mask) st_stream(a.depth_mask + i, (uint8_t)ld);
     if (a.fused_copy) st_stream(a.fused_copy + i, (uint8_t)out);
@@ -450,6 +452,62 @@ __global__ void k_render(const __grid_constant__ SceneFrame sc, uint8_t* R, uint
     if (GT) GT[idx] = label;
 }
 
+// ---------------------------------------------------------------- K2 registration
+// register_mask (registration.cpp:50-78): the same fp64 expression trees,
+// every op an explicit round-to-nearest double intrinsic (no contraction),
+// lround() half away from zero like std::lround.
+__global__ void k_register_splat(const uint8_t* __restrict__ mask,
+                                 const uint16_t* __restrict__ depth, int dw, int dh, size_t n,
+                                 const __grid_constant__ RigDev rig, int cw, int ch,
+                                 uint8_t* __restrict__ out) {
+    const size_t idx = (size_t)blockIdx.x * kThreads + threadIdx.x;
+    if (idx >= n) return;
+    const size_t per = (size_t)dw * dh;
+    const size_t s = idx / per;
+    const int p = (int)(idx - s * per);
+    const int u = p % dw, v = p / dw;
+    if (!mask[idx]) return;
+    const uint32_t raw = depth[idx];
+    if (raw == 0) return;  // no range return, cannot be registered
+    const double z = __dmul_rn((double)raw, rig.scale);
+    const double x = __ddiv_rn(__dmul_rn(__dsub_rn((double)u, rig.dcx), z), rig.dfx);
+    const double y = __ddiv_rn(__dmul_rn(__dsub_rn((double)v, rig.dcy), z), rig.dfy);
+    const double* R = rig.R;
+    const double xc = __dadd_rn(
+        __dadd_rn(__dadd_rn(__dmul_rn(R[0], x), __dmul_rn(R[1], y)), __dmul_rn(R[2], z)), rig.t[0]);
+    const double yc = __dadd_rn(
+        __dadd_rn(__dadd_rn(__dmul_rn(R[3], x), __dmul_rn(R[4], y)), __dmul_rn(R[5], z)), rig.t[1]);
+    const double zc = __dadd_rn(
+        __dadd_rn(__dadd_rn(__dmul_rn(R[6], x), __dmul_rn(R[7], y)), __dmul_rn(R[8], z)), rig.t[2]);
+    if (zc <= 0.0) return;
+    const long uc = lround(__dadd_rn(__ddiv_rn(__dmul_rn(rig.cfx, xc), zc), rig.ccx));
+    const long vc = lround(__dadd_rn(__ddiv_rn(__dmul_rn(rig.cfy, yc), zc), rig.ccy));
+    if (uc < 0 || uc >= cw || vc < 0 || vc >= ch) return;
+    out[s * (size_t)cw * ch + (size_t)vc * cw + uc] = 1;
+}
+
+// dilate_mask (registration.cpp:33-48): OR over a clipped (2r+1)-square,
+// done as a clipped row OR then a clipped column OR.
+template <bool kRows>
+__global__ void k_dilate_pass(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int w,
+                              int h, size_t n, int r) {
+    const size_t idx = (size_t)blockIdx.x * kThreads + threadIdx.x;
+    if (idx >= n) return;
+    const size_t per = (size_t)w * h;
+    const size_t base = (idx / per) * per;
+    const int p = (int)(idx - base);
+    const int x = p % w, y = p / w;
+    uint32_t acc = 0;
+    if (kRows) {
+        const int x0 = max(0, x - r), x1 = min(w - 1, x + r);
+        for (int xx = x0; xx <= x1 && !acc; ++xx) acc |= in[base + (size_t)y * w + xx];
+    } else {
+        const int y0 = max(0, y - r), y1 = min(h - 1, y + r);
+        for (int yy = y0; yy <= y1 && !acc; ++yy) acc |= in[base + (size_t)yy * w + x];
+    }
+    out[idx] = acc ? 1 : 0;
+}
+
 template <typename K, typename... Args>
 cudaError_t go(K kernel, size_t n, cudaStream_t s, Args... args) {
     if (n == 0) return cudaSuccess;
@@ -549,6 +607,25 @@ cudaError_t launch_render(const SceneFrame& sc, uint8_t* r, uint8_t* g, uint8_t*
     k_render<<<blocks_for(n), kThreads, 0, s>>>(sc, r, g, b, d, gt, n);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return cudaGetLastError();
+}
+
+cudaError_t launch_register_splat(const uint8_t* mask, const uint16_t* depth, int dw, int dh,
+                                  int streams, const RigDev& rig, int cw, int ch, uint8_t* out,
+                                  cudaStream_t s) {
+    const size_t n = (size_t)dw * dh * streams;
+    return go(k_register_splat, n, s, mask, depth, dw, dh, n, rig, cw, ch, out);
+}
+
+cudaError_t launch_dilate(const uint8_t* in, uint8_t* tmp, uint8_t* out, int w, int h,
+                          int streams, int radius, cudaStream_t s) {
+    const size_t n = (size_t)w * h * streams;
+    if (radius <= 0) {  // dilate_mask returns the mask unchanged
+        if (out == in) return cudaSuccess;
+        return cudaMemcpyAsync(out, in, n, cudaMemcpyDeviceToDevice, s);
+    }
+    cudaError_t e = go(k_dilate_pass<true>, n, s, in, tmp, w, h, n, radius);
+    if (e != cudaSuccess) return e;
+    return go(k_dilate_pass<false>, n, s, (const uint8_t*)tmp, out, w, h, n, radius);
 }
 
 uint64_t launches() { return g_launches.load(); }

@@ -53,6 +53,7 @@ struct FusedArgs {
     MixCfg ck;
     MixCfg dk;
     int limit;
+    int fuse;  // 0: unregistered sequence -- write rgb/depth masks, fuse after registration
 };
 
 // Kernel variants of K1 (identical results; they differ in HBM writes).
@@ -108,6 +109,26 @@ struct SceneFrame {
 };
 cudaError_t launch_render(const SceneFrame& sc, uint8_t* r, uint8_t* g, uint8_t* b, uint16_t* d,
                           uint8_t* gt, cudaStream_t s);
+
+// Depth->colour registration (registration.cpp:50-78), fp64 exactly as the
+// reference evaluates it.  Rig fields as in CameraRig (registration.hpp:16-26).
+struct RigDev {
+    double dfx, dfy, dcx, dcy;  // depth pinhole
+    double cfx, cfy, ccx, ccy;  // colour pinhole
+    double R[9];                // row-major rotation
+    double t[3];                // translation (mm)
+    double scale;               // depth_scale (mm per raw unit)
+};
+// Splat every valid foreground depth pixel of `streams` frames (dw x dh) into
+// zeroed colour-grid masks (cw x ch); idempotent byte stores.
+cudaError_t launch_register_splat(const uint8_t* mask, const uint16_t* depth, int dw, int dh,
+                                  int streams, const RigDev& rig, int cw, int ch, uint8_t* out,
+                                  cudaStream_t s);
+// Square binary dilation of radius r (dilate_mask, registration.cpp:33-48) as
+// a row pass then a column pass (exact for a square structuring element with
+// the reference's border clipping).  tmp: scratch of the same size.
+cudaError_t launch_dilate(const uint8_t* in, uint8_t* tmp, uint8_t* out, int w, int h,
+                          int streams, int radius, cudaStream_t s);
 
 uint64_t launches();
 

@@ -112,6 +112,7 @@ class RunConfig:
     depth_gmm: MixtureConfig = field(default_factory=MixtureConfig)
     fusion_counter_limit: int = 3
     fusion_initial_label: int = 0
+    dilation_radius: int = 1
     warmup_frames: int = 30
 
     @staticmethod
@@ -128,6 +129,7 @@ class RunConfig:
             "depth_gmm": self.depth_gmm.to_dict(),
             "fusion": {"counter_limit": self.fusion_counter_limit,
                        "initial_label": self.fusion_initial_label},
+            "registration": {"dilation_radius": self.dilation_radius},
             "evaluation": {"warmup_frames": self.warmup_frames},
         }, indent=2)
 
@@ -434,6 +436,69 @@ def reset_state(width: int, height: int, initial_label: int = 0, counter_limit: 
     return FusionState(width, height, initial_label, counter_limit)
 
 
+# ------------------------------------------------------------------ registration
+
+class CameraRig:
+    """CameraRig (registration.hpp:16-26; module.cpp:92-98): depth and colour
+    pinholes, row-major rotation, translation in mm, depth_scale."""
+
+    def __init__(self):
+        self.depth_cam = [0.0, 0.0, 0.0, 0.0]  # fx, fy, cx, cy
+        self.color_cam = [0.0, 0.0, 0.0, 0.0]
+        self.rotation = [1.0, 0.0, 0.0, 0.0, 1.0, 0.0, 0.0, 0.0, 1.0]
+        self.translation_mm = [0.0, 0.0, 0.0]
+        self.depth_scale = 1.0
+
+    @staticmethod
+    def identity(fx=525.0, fy=525.0, cx=319.5, cy=239.5) -> "CameraRig":
+        r = CameraRig()
+        r.depth_cam = [fx, fy, cx, cy]
+        r.color_cam = [fx, fy, cx, cy]
+        return r
+
+    def _c(self) -> _lib.CameraRigC:
+        c = _lib.CameraRigC()
+        c.depth_fx, c.depth_fy, c.depth_cx, c.depth_cy = map(float, self.depth_cam)
+        c.color_fx, c.color_fy, c.color_cx, c.color_cy = map(float, self.color_cam)
+        for i in range(9):
+            c.rotation[i] = float(self.rotation[i])
+        for i in range(3):
+            c.translation_mm[i] = float(self.translation_mm[i])
+        c.depth_scale = float(self.depth_scale)
+        return c
+
+    def validate(self):
+        c = self._c()
+        check(lib.rgbdseg_camera_rig_validate(C.byref(c)))
+
+
+def register_mask(mask, depth, rig: CameraRig, dilation_radius: int = 1, color_width=None,
+                  color_height=None, device: int = 0):
+    """register_mask (registration.cpp:50-78; module.cpp:100-110) on the GPU:
+    the colour-grid mask of the foreground depth pixels, dilated."""
+    _check_mask(mask)
+    m = _as_host(mask, np.uint8, np.shape(mask))
+    h, w = m.shape[-2:]
+    d = _as_host(depth, np.uint16, (h, w))
+    cw, ch = color_width or w, color_height or h
+    out = np.empty((ch, cw), np.uint8)
+    c = rig._c()
+    check(lib.rgbdseg_register_mask(_buf(m, np.uint8, w * h, "mask"),
+                                    _buf(d, np.uint16, w * h, "depth"), w, h, C.byref(c), cw, ch,
+                                    int(dilation_radius), out.ctypes.data, device))
+    return out
+
+
+def dilate_mask(mask, radius: int, device: int = 0):
+    """dilate_mask (registration.cpp:33-48) on the GPU."""
+    m = _as_host(mask, np.uint8, np.shape(mask))
+    h, w = m.shape[-2:]
+    out = np.empty((h, w), np.uint8)
+    check(lib.rgbdseg_dilate_mask(_buf(m, np.uint8, w * h, "mask"), w, h, int(radius),
+                                  out.ctypes.data, device))
+    return out
+
+
 # ------------------------------------------------------------------ processor
 
 @dataclass
@@ -452,7 +517,8 @@ class SequenceProcessor:
     into one fused kernel per step."""
 
     def __init__(self, width: int, height: int, config: Optional[RunConfig] = None,
-                 streams: int = 1, device: int = 0, variant: str = "auto", host_chunks: int = 0):
+                 streams: int = 1, device: int = 0, variant: str = "auto", host_chunks: int = 0,
+                 rig: Optional[CameraRig] = None, registered: bool = True):
         config = config or RunConfig.defaults()
         self.width, self.height, self.streams, self.device = width, height, streams, device
         self.config = config
@@ -465,6 +531,12 @@ class SequenceProcessor:
         pc.fusion_initial_label = int(config.fusion_initial_label)
         pc.device = device
         pc.host_chunks = host_chunks
+        pc.registered = 1 if registered else 0
+        pc.dilation_radius = int(config.dilation_radius)
+        if not registered:
+            if rig is None:  # processor.cpp:131-132
+                raise ValueError("unregistered sequence requires calibration")
+            pc.rig = rig._c()
         h = C.c_void_p()
         check(lib.rgbdseg_processor_create(C.byref(pc), C.byref(h)), "SequenceProcessor")
         self._h = h.value

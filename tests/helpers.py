@@ -41,3 +41,21 @@ def sha256(*arrs) -> str:
     for a in arrs:
         h.update(np.ascontiguousarray(a).tobytes())
     return h.hexdigest()
+
+
+def random_rig(rng, w, h, big=False):
+    """A valid CameraRig as 21 doubles: pinholes near (w/2, h/2), a small
+    Rodrigues rotation (orthonormal to ~1e-16) and a translation in mm."""
+    fx, fy = rng.uniform(400, 600, 2)
+    cfx, cfy = fx * rng.uniform(0.95, 1.05), fy * rng.uniform(0.95, 1.05)
+    dcx, dcy = w / 2 + rng.uniform(-3, 3), h / 2 + rng.uniform(-3, 3)
+    ccx, ccy = w / 2 + rng.uniform(-3, 3), h / 2 + rng.uniform(-3, 3)
+    axis = rng.normal(size=3)
+    axis /= np.linalg.norm(axis)
+    ang = rng.uniform(0, 0.2 if big else 0.03)
+    K = np.array([[0, -axis[2], axis[1]], [axis[2], 0, -axis[0]], [-axis[1], axis[0], 0]])
+    Rm = np.eye(3) + np.sin(ang) * K + (1 - np.cos(ang)) * (K @ K)
+    t = rng.uniform(-60, 60, 3)
+    scale = rng.choice([1.0, 0.5, 1.25])
+    return np.ascontiguousarray([fx, fy, dcx, dcy, cfx, cfy, ccx, ccy, *Rm.ravel(), *t, scale],
+                                np.float64)

@@ -478,3 +478,91 @@ def test_cpp_dropin_matches_reference_sequence_processor(cuda):
         print(r.stdout)
         assert r.returncode == 0, r.stdout + r.stderr
         assert "banks identical" in r.stdout
+
+
+# ------------------------------------------------------------ K2 registration
+
+def _rig_from_array(R, a):
+    rig = R.CameraRig()
+    rig.depth_cam, rig.color_cam = list(a[0:4]), list(a[4:8])
+    rig.rotation, rig.translation_mm, rig.depth_scale = list(a[8:17]), list(a[17:20]), float(a[20])
+    return rig
+
+
+def test_register_mask_matches_oracle(R, port):
+    """register_mask (registration.cpp:50-78) on the GPU against the oracle
+    (pinned to the reference): 80 random rigs, holes, radii 0..3, plus the
+    reference's hand cases (test_registration.cpp:22-67)."""
+    from helpers import random_rig
+    from test_oracle import _port_register
+
+    rng = np.random.default_rng(33)
+    for trial in range(80):
+        w, h = int(rng.integers(20, 200)), int(rng.integers(16, 150))
+        a = random_rig(rng, w, h, big=trial % 3 == 0)
+        mask = (rng.random((h, w)) < 0.3).astype(np.uint8)
+        depth = rng.integers(0, 5000, (h, w)).astype(np.uint16)
+        depth[rng.random((h, w)) < 0.1] = 0
+        radius = int(trial % 4)
+        got = R.register_mask(mask, depth, _rig_from_array(R, a), dilation_radius=radius)
+        assert np.array_equal(got, _port_register(port, mask, depth, a, w, h, radius)), trial
+    # identity rig, radius 0 is the identity on valid masks (test_smoke.py:52-58)
+    mask = np.zeros((24, 32), np.uint8)
+    mask[10:14, 5:9] = 1
+    out = R.register_mask(mask, np.full((24, 32), 1500, np.uint16), R.CameraRig.identity(),
+                          dilation_radius=0)
+    assert np.array_equal(out, mask)
+    # fx=500, z=1000 mm, t=(50,0,0): (320,240) -> (345,240)
+    rig = R.CameraRig()
+    rig.depth_cam = rig.color_cam = [500, 500, 320, 240]
+    rig.translation_mm = [50, 0, 0]
+    one = np.zeros((480, 640), np.uint8)
+    one[240, 320] = 1
+    out = R.register_mask(one, np.full((480, 640), 1000, np.uint16), rig, dilation_radius=0)
+    assert out[240, 345] == 1 and out.sum() == 1
+    bad = R.CameraRig.identity()
+    bad.rotation = [1, 0.5, 0, 0, 1, 0, 0, 0, 1]
+    with pytest.raises(ValueError, match="orthonormal"):
+        R.register_mask(one, np.full((480, 640), 1000, np.uint16), bad)
+
+
+def test_dilate_mask_matches_oracle(R, port):
+    rng = np.random.default_rng(2)
+    for r in (0, 1, 2, 5):
+        m = (rng.random((57, 83)) < 0.05).astype(np.uint8)
+        exp = np.empty_like(m)
+        port.lib.orc_dilate(m, exp, 83, 57, r)
+        assert np.array_equal(R.dilate_mask(m, r), exp), r
+
+
+@pytest.mark.parametrize("streams", [1, 3])
+def test_unregistered_processor_matches_oracle(R, port, streams):
+    """processor.cpp:175-179 on the GPU: K1 without fusion, splat, dilation,
+    List 1 -- against the oracle's unregistered processor per stream."""
+    from helpers import random_rig
+
+    rng = np.random.default_rng(5)
+    w, h, M = 96, 72, 5
+    a = random_rig(rng, w, h)
+    cfg = R.RunConfig.defaults()
+    cfg.color_gmm.components = cfg.depth_gmm.components = M
+    cfg.dilation_radius = 2
+    proc = R.SequenceProcessor(w, h, cfg, streams=streams, rig=_rig_from_array(R, a),
+                               registered=False)
+    orc = [O.PortProcessor(port, w * h, O.color_cfg(M), O.depth_cfg(M), rig=a, width=w, height=h,
+                           radius=2) for _ in range(streams)]
+    scenes = [O.PortScene(port, "A", w, h, seed=s + 1) for s in range(streams)]
+    for f in range(40):
+        frs = [sc.render(f) for sc in scenes]
+        r, g, b = (np.stack([getattr(x, k) for x in frs]) for k in ("r", "g", "b"))
+        d = np.stack([holes(x.depth, f) for x in frs])
+        fm = proc.process(r[0] if streams == 1 else r, g[0] if streams == 1 else g,
+                          b[0] if streams == 1 else b, d[0] if streams == 1 else d)
+        for s in range(streams):
+            rgb, dep, fu = orc[s].process(r[s], g[s], b[s], d[s])
+            sel = (lambda x: x) if streams == 1 else (lambda x, s=s: x[s])
+            assert np.array_equal(sel(fm.rgb).ravel(), rgb), (f, s)
+            assert np.array_equal(sel(fm.depth).ravel(), dep), (f, s)
+            assert np.array_equal(sel(fm.fused).ravel(), fu), (f, s)
+    with pytest.raises(ValueError, match="calibration"):
+        R.SequenceProcessor(w, h, cfg, registered=False)

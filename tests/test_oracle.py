@@ -184,3 +184,79 @@ def test_fusion_exhaustive_port(port):
         port.lib.orc_fuse(out, cpt, 8192, 3, np.ascontiguousarray(rgb[s]),
                           np.ascontiguousarray(dep[s]))
         assert np.array_equal(out, eo[s]) and np.array_equal(cpt, ec[s])
+
+
+# ---- registration (registration.cpp:33-78; test_registration.cpp) ----------
+
+def _port_register(port, mask, depth, rig, cw, ch, radius):
+    h, w = mask.shape
+    out = np.empty(cw * ch, np.uint8)
+    scratch = np.empty(cw * ch, np.uint8)
+    port.lib.orc_register(np.ascontiguousarray(mask).ravel(), np.ascontiguousarray(depth).ravel(),
+                          w, h, rig, cw, ch, radius, scratch, out)
+    return out.reshape(ch, cw)
+
+
+def _ref_register(ref, mask, depth, rig, cw, ch, radius):
+    h, w = mask.shape
+    out = np.empty(cw * ch, np.uint8)
+    ref.check(ref.lib.rref_register_mask(np.ascontiguousarray(mask).ravel(),
+                                         np.ascontiguousarray(depth).ravel(), w, h, rig, cw, ch,
+                                         radius, out))
+    return out.reshape(ch, cw)
+
+
+def test_port_registration_reference_cases(port):
+    ident = O.rig_array([525, 525, 319.5, 239.5], [525, 525, 319.5, 239.5],
+                        [1, 0, 0, 0, 1, 0, 0, 0, 1], [0, 0, 0], 1.0)
+    rng = np.random.default_rng(4)
+    mask = (rng.integers(0, 5, (48, 64)) == 0).astype(np.uint8)
+    depth = (500 + rng.integers(0, 3000, (48, 64))).astype(np.uint16)
+    assert np.array_equal(_port_register(port, mask, depth, ident, 64, 48, 0), mask)
+    off = O.rig_array([500, 500, 320, 240], [500, 500, 320, 240], [1, 0, 0, 0, 1, 0, 0, 0, 1],
+                      [50, 0, 0], 1.0)
+    one = np.zeros((480, 640), np.uint8)
+    one[240, 320] = 1
+    out = _port_register(port, one, np.full((480, 640), 1000, np.uint16), off, 640, 480, 0)
+    assert out[240, 345] == 1 and out.sum() == 1  # test_registration.cpp:36-48
+    assert not _port_register(port, np.ones((16, 16), np.uint8), np.zeros((16, 16), np.uint16),
+                              ident, 16, 16, 1).any()
+    far = off.copy()
+    far[17] = 100000
+    assert not _port_register(port, np.ones((48, 64), np.uint8),
+                              np.full((48, 64), 1000, np.uint16), far, 64, 48, 0).any()
+
+
+def test_port_registration_matches_reference(port, ref):
+    from helpers import random_rig
+
+    rng = np.random.default_rng(21)
+    for trial in range(60):
+        w, h = int(rng.integers(20, 90)), int(rng.integers(16, 70))
+        rig = random_rig(rng, w, h, big=trial % 3 == 0)
+        mask = (rng.random((h, w)) < 0.3).astype(np.uint8)
+        depth = rng.integers(0, 5000, (h, w)).astype(np.uint16)
+        depth[rng.random((h, w)) < 0.1] = 0
+        radius = int(trial % 4)
+        a = _port_register(port, mask, depth, rig, w, h, radius)
+        b = _ref_register(ref, mask, depth, rig, w, h, radius)
+        assert np.array_equal(a, b), trial
+
+
+def test_port_unregistered_processor_matches_reference(port, ref):
+    """processor.cpp:175-179: registration + dilation between the depth bank
+    and fusion; 40 frames of scenario A with a rig, M=4."""
+    from helpers import random_rig
+
+    rng = np.random.default_rng(8)
+    w, h, M = 96, 72, 4
+    rig = random_rig(rng, w, h)
+    pp = O.PortProcessor(port, w * h, O.color_cfg(M), O.depth_cfg(M), rig=rig, width=w, height=h,
+                         radius=2)
+    rp = O.RefProcessor(ref, w, h, O.color_cfg(M), O.depth_cfg(M), workers=2, rig=rig, radius=2)
+    sc = O.PortScene(port, "A", w, h)
+    for f in range(40):
+        fr = sc.render(f)
+        d = holes(fr.depth, f)
+        for x, y in zip(pp.process(fr.r, fr.g, fr.b, d), rp.process(fr.r, fr.g, fr.b, d)):
+            assert np.array_equal(x, y), f
