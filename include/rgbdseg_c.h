@@ -40,8 +40,8 @@ typedef enum {
     RGBDSEG_ERUNTIME = 4
 } rgbdseg_status;
 
-/* Bank modes, segmenter.hpp:11 (Augmented4 is not on this path). */
-enum { RGBDSEG_COLOR3 = 0, RGBDSEG_DEPTH1 = 1 };
+/* Bank modes, segmenter.hpp:11 */
+enum { RGBDSEG_COLOR3 = 0, RGBDSEG_DEPTH1 = 1, RGBDSEG_AUGMENTED4 = 2 };
 
 /* MixtureConfig, mixture.hpp:16-26 -- same fields, same order, same defaults
  * (rgbdseg_mixture_defaults). */
@@ -123,6 +123,13 @@ int rgbdseg_segment_color(rgbdseg_bank* bank, const uint8_t* r, const uint8_t* g
                           const uint8_t* b, const rgbdseg_mixture_cfg* cfg, uint8_t* mask_out);
 int rgbdseg_segment_depth(rgbdseg_bank* bank, const uint16_t* depth_mm,
                           const rgbdseg_mixture_cfg* cfg, uint8_t* mask_out);
+
+/* segment_augmented, segmenter.cpp:133-147: one 4-channel mixture over
+ * (R, G, B, DepthRescale{min_mm, max_mm}.to_channel(depth)); no depth
+ * sentinel.  min_mm < max_mm (RunConfig::validate, processor.cpp:56-57). */
+int rgbdseg_segment_augmented(rgbdseg_bank* bank, const uint8_t* r, const uint8_t* g,
+                              const uint8_t* b, const uint16_t* depth_mm, float min_mm,
+                              float max_mm, const rgbdseg_mixture_cfg* cfg, uint8_t* mask_out);
 
 /* ---- FusionState / reset_state / fuse_step: fusion.hpp:11-23 ----------- */
 int rgbdseg_fusion_create(int width, int height, int streams, int initial_label,

@@ -8,9 +8,8 @@
 // Same constructor arguments, same process(FrameSet&&) -> FrameMasks contract
 // (processor.cpp:158-184), same exception types; the banks stay in HBM and
 // color_bank()/depth_bank() return host ModelBank copies (the reference
-// returns const pointers into host state).  Scope: registered sequences,
-// methods rgb/depth/fused (the GPU path of DESIGN.md); augmented and
-// unregistered sequences throw std::invalid_argument.
+// returns const pointers into host state).  Every MethodSet combination and
+// unregistered sequences (rig + depth->colour registration) are served.
 #pragma once
 
 #include <optional>
@@ -58,10 +57,6 @@ public:
         config_.validate();  // processor.cpp:128
         if (!registered && !rig)
             throw std::invalid_argument("unregistered sequence requires calibration");
-        if (!registered)
-            throw std::invalid_argument("b200: depth->colour registration is not on the GPU path yet");
-        if (methods_.augmented)
-            throw std::invalid_argument("b200: the augmented method is not on the GPU path");
         rgbdseg_processor_cfg c;
         rgbdseg_processor_defaults(&c, width, height);
         c.color = to_c(config_.color_gmm);
@@ -69,9 +64,26 @@ public:
         c.fusion_counter_limit = config_.fusion_counter_limit;
         c.fusion_initial_label = config_.fusion_initial_label;
         c.device = device;
+        c.registered = registered ? 1 : 0;
+        c.dilation_radius = config_.dilation_radius;
+        if (rig) {
+            c.rig = rgbdseg_camera_rig{rig->depth_cam.fx, rig->depth_cam.fy, rig->depth_cam.cx,
+                                       rig->depth_cam.cy, rig->color_cam.fx, rig->color_cam.fy,
+                                       rig->color_cam.cx, rig->color_cam.cy, {}, {},
+                                       rig->depth_scale};
+            for (int i = 0; i < 9; ++i) c.rig.rotation[i] = rig->rotation[i];
+            for (int i = 0; i < 3; ++i) c.rig.translation_mm[i] = rig->translation_mm[i];
+        }
         check(rgbdseg_processor_create(&c, &p_));
+        if (methods_.augmented) {  // segment_augmented's own bank (processor.cpp:148-150)
+            const rgbdseg_mixture_cfg a = to_c(config_.augmented_gmm);
+            check(rgbdseg_bank_create(width, height, 1, RGBDSEG_AUGMENTED4, &a, device, &aug_));
+        }
     }
-    ~SequenceProcessor() { rgbdseg_processor_destroy(p_); }
+    ~SequenceProcessor() {
+        rgbdseg_processor_destroy(p_);
+        rgbdseg_bank_destroy(aug_);
+    }
     SequenceProcessor(const SequenceProcessor&) = delete;
     SequenceProcessor& operator=(const SequenceProcessor&) = delete;
 
@@ -86,6 +98,14 @@ public:
         if (methods_.needs_rgb()) out.rgb = std::move(rgb);
         if (methods_.needs_depth()) out.depth = std::move(dep);
         if (methods_.fused) out.fused = std::move(fused);
+        if (aug_) {
+            MaskPlane am(w_, h_);
+            const rgbdseg_mixture_cfg a = to_c(config_.augmented_gmm);
+            check(rgbdseg_segment_augmented(aug_, frame.r.data(), frame.g.data(), frame.b.data(),
+                                            frame.depth.data(), config_.augmented_depth_range.min_mm,
+                                            config_.augmented_depth_range.max_mm, &a, am.data()));
+            out.augmented = std::move(am);
+        }
         out.gt = std::move(frame.gt);
         return out;
     }
@@ -104,6 +124,7 @@ private:
     MethodSet methods_;
     RunConfig config_;
     rgbdseg_processor* p_ = nullptr;
+    rgbdseg_bank* aug_ = nullptr;
 };
 
 }  // namespace rgbdseg::b200

@@ -108,6 +108,8 @@ class Port:
         L.orc_segment_color.argtypes = [_f32p, _u8p, C.c_size_t, _u8p, _u8p, _u8p,
                                         C.POINTER(Cfg), _u8p]
         L.orc_segment_depth.argtypes = [_f32p, _u8p, C.c_size_t, _u16p, C.POINTER(Cfg), _u8p]
+        L.orc_segment_augmented.argtypes = [_f32p, _u8p, C.c_size_t, _u8p, _u8p, _u8p, _u16p,
+                                            C.c_float, C.c_float, C.POINTER(Cfg), _u8p]
         L.orc_fusion_reset.argtypes = [_u8p, _i8p, C.c_size_t, C.c_uint8]
         L.orc_fuse.argtypes = [_u8p, _i8p, C.c_size_t, C.c_int, _u8p, _u8p]
         L.orc_register.argtypes = [_u8p, _u16p, C.c_int, C.c_int, _f64p, C.c_int, C.c_int,
@@ -190,6 +192,13 @@ class PortBank:
                                         C.byref(self.cfg), mask)
         return mask
 
+    def segment_augmented(self, r, g, b, d, lo=0.0, hi=4000.0) -> np.ndarray:
+        mask = np.empty(self.npx, np.uint8)
+        rav = [np.ascontiguousarray(x).ravel() for x in (r, g, b, d)]
+        self.port.lib.orc_segment_augmented(self.state, self.flags, self.npx, *rav, lo, hi,
+                                            C.byref(self.cfg), mask)
+        return mask
+
     def segment_depth(self, d) -> np.ndarray:
         mask = np.empty(self.npx, np.uint8)
         self.port.lib.orc_segment_depth(self.state, self.flags, self.npx,
@@ -253,6 +262,8 @@ class Ref:
         L.rref_segment_color.argtypes = [C.c_void_p, _u8p, _u8p, _u8p, C.POINTER(Cfg), C.c_int,
                                          _u8p]
         L.rref_segment_depth.argtypes = [C.c_void_p, _u16p, C.POINTER(Cfg), C.c_int, _u8p]
+        L.rref_segment_augmented.argtypes = [C.c_void_p, _u8p, _u8p, _u8p, _u16p, C.c_float,
+                                             C.c_float, C.POINTER(Cfg), C.c_int, _u8p]
         L.rref_bank_get.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p]
         L.rref_bank_set.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p]
         L.rref_fusion_create.restype = C.c_void_p

@@ -156,7 +156,11 @@ int rref_match_component(const RefMix* m, const float* v, const RefCfg* c, int* 
 // ---- banks (segmenter.hpp:25-69) ----
 void* rref_bank_create(int w, int h, int mode, const RefCfg* c) {
     try {
-        return new ModelBank(w, h, mode == 0 ? BankMode::Color3 : BankMode::Depth1, to_ref(c));
+        return new ModelBank(w, h,
+                             mode == 0   ? BankMode::Color3
+                             : mode == 1 ? BankMode::Depth1
+                                         : BankMode::Augmented4,
+                             to_ref(c));
     } catch (const std::exception& e) {
         g_err = e.what();
         return nullptr;
@@ -181,6 +185,19 @@ int rref_segment_depth(void* bank, const uint16_t* d, const RefCfg* c, int worke
         auto* bk = static_cast<ModelBank*>(bank);
         const MaskPlane m =
             segment_depth(*bk, plane_of(d, bk->width(), bk->height()), to_ref(c), workers);
+        std::memcpy(mask, m.data(), m.size());
+    });
+}
+
+int rref_segment_augmented(void* bank, const uint8_t* r, const uint8_t* g, const uint8_t* b,
+                           const uint16_t* d, float lo, float hi, const RefCfg* c, int workers,
+                           uint8_t* mask) {
+    return guard([&] {
+        auto* bk = static_cast<ModelBank*>(bank);
+        const int w = bk->width(), h = bk->height();
+        const MaskPlane m = segment_augmented(*bk, plane_of(r, w, h), plane_of(g, w, h),
+                                              plane_of(b, w, h), plane_of(d, w, h),
+                                              DepthRescale{lo, hi}, to_ref(c), workers);
         std::memcpy(mask, m.data(), m.size());
     });
 }

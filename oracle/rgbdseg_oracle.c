@@ -250,6 +250,24 @@ void orc_segment_depth(float* state, uint8_t* flags, size_t npx, const uint16_t*
     }
 }
 
+/* DepthRescale::to_channel, segmenter.cpp:18-22 */
+static float orc_to_channel(float d, float lo, float hi) {
+    if (d <= lo) return 0.0f;
+    if (d >= hi) return 255.0f;
+    return (d - lo) * 255.0f / (hi - lo);
+}
+
+/* segment_augmented, segmenter.cpp:133-147: 4 channels, no depth sentinel. */
+void orc_segment_augmented(float* state, uint8_t* flags, size_t npx, const uint8_t* r,
+                           const uint8_t* g, const uint8_t* b, const uint16_t* depth, float lo,
+                           float hi, const orc_cfg* k, uint8_t* mask) {
+    for (size_t j = 0; j < npx; ++j) {
+        const float v[4] = {(float)r[j], (float)g[j], (float)b[j],
+                            orc_to_channel((float)depth[j], lo, hi)};
+        mask[j] = orc_bank_pixel(state, flags, npx, j, 4, v, 1, k);
+    }
+}
+
 /* ------------------------------------------------------------------------
  * List-1 fusion, fusion.cpp:7-46.  cpt is int8 (fusion.hpp:13).
  * ---------------------------------------------------------------------- */

@@ -7,6 +7,7 @@ from .rgbdseg import (  # noqa: F401
     PIXEL_MIXTURE_DTYPE,
     BankMode,
     CameraRig,
+    DepthRescale,
     FrameMasks,
     FusionState,
     MixtureConfig,
@@ -25,6 +26,7 @@ from .rgbdseg import (  # noqa: F401
     reset_state,
     segment_color,
     segment_depth,
+    segment_augmented,
     step_mixtures,
     step_pixel,
 )

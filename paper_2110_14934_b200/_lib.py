@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("RGBDSEG_B200_LIB", os.path.join(HERE, "librgbdseg_b200.so"))
 
 OK, EINVAL, ECUDA, ENOMEM, ERUNTIME = 0, 1, 2, 3, 4
-COLOR3, DEPTH1 = 0, 1
+COLOR3, DEPTH1, AUGMENTED4 = 0, 1, 2
 FLAGS_PLANE = -1
 VARIANTS = {"auto": 0, "ldg": 1, "ldg_elide": 2}
 
@@ -89,6 +89,8 @@ SIGNATURES = {
     "rgbdseg_bank_device_ptrs": (_i, [_vp, C.POINTER(_vp), C.POINTER(_sz), C.POINTER(_sz)]),
     "rgbdseg_segment_color": (_i, [_vp, _vp, _vp, _vp, C.POINTER(MixtureCfg), _vp]),
     "rgbdseg_segment_depth": (_i, [_vp, _vp, C.POINTER(MixtureCfg), _vp]),
+    "rgbdseg_segment_augmented": (_i, [_vp, _vp, _vp, _vp, _vp, C.c_float, C.c_float,
+                                       C.POINTER(MixtureCfg), _vp]),
     "rgbdseg_fusion_create": (_i, [_i, _i, _i, _i, _i, _i, C.POINTER(_vp)]),
     "rgbdseg_fusion_destroy": (None, [_vp]),
     "rgbdseg_fusion_step": (_i, [_vp, _vp, _vp, _vp]),

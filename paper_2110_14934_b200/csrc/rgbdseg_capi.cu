@@ -288,7 +288,7 @@ int rgbdseg_bank_create(int width, int height, int streams, int mode,
                         const rgbdseg_mixture_cfg* cfg, int device, rgbdseg_bank** out) {
     *out = nullptr;
     if (int rc = check_dims(width, height, streams)) return rc;
-    if (mode != RGBDSEG_COLOR3 && mode != RGBDSEG_DEPTH1)
+    if (mode != RGBDSEG_COLOR3 && mode != RGBDSEG_DEPTH1 && mode != RGBDSEG_AUGMENTED4)
         return fail(RGBDSEG_EINVAL, "unknown bank mode");
     if (int rc = validate_cfg(cfg)) return rc;  // segmenter.cpp:26
     GUARD(device);
@@ -298,7 +298,7 @@ int rgbdseg_bank_create(int width, int height, int streams, int mode,
     b->streams = streams;
     b->mode = mode;
     b->M = cfg->components;
-    b->C = mode == RGBDSEG_COLOR3 ? 3 : 1;
+    b->C = mode == RGBDSEG_COLOR3 ? 3 : (mode == RGBDSEG_DEPTH1 ? 1 : 4);
     b->device = device;
     b->cfg = *cfg;
     b->npx = (size_t)width * height * streams;
@@ -375,9 +375,9 @@ static int bank_call_checks(const rgbdseg_bank* b, const rgbdseg_mixture_cfg* cf
                             const char* who) {
     if (!b) return fail(RGBDSEG_EINVAL, std::string(who) + ": null bank");
     if (b->mode != mode)
-        return fail(RGBDSEG_EINVAL, std::string(who) + (mode == RGBDSEG_COLOR3
-                                                            ? ": bank mode is not Color3"
-                                                            : ": bank mode is not Depth1"));
+        return fail(RGBDSEG_EINVAL, std::string(who) + (mode == RGBDSEG_COLOR3   ? ": bank mode is not Color3"
+                                                        : mode == RGBDSEG_DEPTH1 ? ": bank mode is not Depth1"
+                                                                                 : ": bank mode is not Augmented4"));
     if (int rc = validate_cfg(cfg)) return rc;
     if (cfg->components != b->M)
         return fail(RGBDSEG_EINVAL, "segment: config component count does not match bank");
@@ -431,6 +431,33 @@ int rgbdseg_segment_depth(rgbdseg_bank* b, const uint16_t* depth_mm,
         }
     }
     CU(launch_bank_depth(b->view(), to_k(*cfg), (const uint16_t*)dd, dm, b->npx, b->stream));
+    return finish_mask(dm, mask_out, b->npx, b->stream);
+}
+
+int rgbdseg_segment_augmented(rgbdseg_bank* b, const uint8_t* r, const uint8_t* g,
+                              const uint8_t* bl, const uint16_t* depth_mm, float min_mm,
+                              float max_mm, const rgbdseg_mixture_cfg* cfg, uint8_t* mask_out) {
+    if (int rc = bank_call_checks(b, cfg, RGBDSEG_AUGMENTED4, "segment_augmented")) return rc;
+    if (!(max_mm > min_mm)) return fail(RGBDSEG_EINVAL, "config: augmented depth range is empty");
+    GUARD(b->device);
+    const void *dr, *dg, *db, *dd;
+    if (int rc = stage_in(r, b->npx, b->s_r, &dr, b->stream)) return rc;
+    if (int rc = stage_in(g, b->npx, b->s_g, &dg, b->stream)) return rc;
+    if (int rc = stage_in(bl, b->npx, b->s_b, &db, b->stream)) return rc;
+    if (int rc = stage_in(depth_mm, b->npx * 2, b->s_plane, &dd, b->stream)) return rc;
+    uint8_t* dm = nullptr;
+    if (mask_out) {
+        if (on_device(mask_out)) {
+            dm = mask_out;
+        } else {
+            void* p;
+            if (int rc = b->s_mask.get(b->npx, &p)) return rc;
+            dm = static_cast<uint8_t*>(p);
+        }
+    }
+    CU(launch_bank_aug(b->view(), to_k(*cfg), (const uint8_t*)dr, (const uint8_t*)dg,
+                       (const uint8_t*)db, (const uint16_t*)dd, min_mm, max_mm, dm, b->npx,
+                       b->stream));
     return finish_mask(dm, mask_out, b->npx, b->stream);
 }
 

@@ -236,6 +236,38 @@ __global__ void __launch_bounds__(kThreads)
     if (mask) mask[j] = (uint8_t)lab;
 }
 
+// DepthRescale::to_channel (segmenter.cpp:18-22): metric depth onto 0..255.
+__device__ __forceinline__ float rescale_depth(float d, float lo, float hi) {
+    if (d <= lo) return 0.0f;
+    if (d >= hi) return 255.0f;
+    return fdiv(fmul(fsub(d, lo), 255.0f), fsub(hi, lo));
+}
+
+// segment_augmented (segmenter.cpp:133-147): one 4-channel mixture over
+// (R, G, B, rescaled depth).  No no-return sentinel here: raw 0 rescales to
+// channel value 0 and is modelled like any other observation.
+template <int M>
+__global__ void __launch_bounds__(kThreads)
+    k_bank_aug(BankView bk, MixCfg k, const uint8_t* __restrict__ r,
+               const uint8_t* __restrict__ g, const uint8_t* __restrict__ b,
+               const uint16_t* __restrict__ d, float lo, float hi, uint8_t* __restrict__ mask,
+               size_t n) {
+    const size_t j = (size_t)blockIdx.x * kThreads + threadIdx.x;
+    if (j >= n) return;
+    const float v[4] = {(float)r[j], (float)g[j], (float)b[j],
+                        rescale_depth((float)d[j], lo, hi)};
+    float* st = px_base<M, 4>(bk, j);
+    uint8_t* fl = px_flag<M, 4>(bk, j);
+    const bool init = *fl != 0;
+    Mixture<M, 4> m;
+    load_mix(st, m);
+    int t;
+    const uint32_t lab = bank_pixel(m, st, v, init, k, t);
+    store_mix(st, m);
+    if (!init) *fl = 1;
+    if (mask) mask[j] = (uint8_t)lab;
+}
+
 // ModelBank ctor state (segmenter.cpp:24-34): means 0, var sigma0^2, w (1,0,..)
 __global__ void k_bank_reset(BankView bk, float sigma0, size_t n) {
     const size_t j = (size_t)blockIdx.x * kThreads + threadIdx.x;
@@ -569,6 +601,17 @@ cudaError_t launch_bank_depth(BankView bk, const MixCfg& k, const uint16_t* d, u
         case 3: return go(k_bank_depth<3>, n, s, bk, k, d, mask, n);
         case 4: return go(k_bank_depth<4>, n, s, bk, k, d, mask, n);
         case 5: return go(k_bank_depth<5>, n, s, bk, k, d, mask, n);
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_bank_aug(BankView bk, const MixCfg& k, const uint8_t* r, const uint8_t* g,
+                            const uint8_t* b, const uint16_t* d, float lo, float hi,
+                            uint8_t* mask, size_t n, cudaStream_t s) {
+    switch (bk.M) {
+        case 3: return go(k_bank_aug<3>, n, s, bk, k, r, g, b, d, lo, hi, mask, n);
+        case 4: return go(k_bank_aug<4>, n, s, bk, k, r, g, b, d, lo, hi, mask, n);
+        case 5: return go(k_bank_aug<5>, n, s, bk, k, r, g, b, d, lo, hi, mask, n);
     }
     return cudaErrorInvalidValue;
 }

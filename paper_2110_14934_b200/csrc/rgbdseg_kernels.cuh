@@ -67,6 +67,9 @@ cudaError_t launch_bank_color(BankView bank, const MixCfg& k, const uint8_t* r, 
                               const uint8_t* b, uint8_t* mask, size_t n, cudaStream_t s);
 cudaError_t launch_bank_depth(BankView bank, const MixCfg& k, const uint16_t* d, uint8_t* mask,
                               size_t n, cudaStream_t s);
+cudaError_t launch_bank_aug(BankView bank, const MixCfg& k, const uint8_t* r, const uint8_t* g,
+                            const uint8_t* b, const uint16_t* d, float lo, float hi,
+                            uint8_t* mask, size_t n, cudaStream_t s);
 cudaError_t launch_bank_reset(BankView bank, float sigma0, size_t n, cudaStream_t s);
 // plane = ModelBank plane id, or -1 for the flags (uint8).  dst/src: npx elements.
 cudaError_t launch_bank_gather(BankView bank, int plane, size_t n, void* dst, cudaStream_t s);

@@ -231,6 +231,15 @@ def step_pixel(mix: PixelMixture, value, cfg: MixtureConfig) -> int:
 class BankMode:
     Color3 = _lib.COLOR3
     Depth1 = _lib.DEPTH1
+    Augmented4 = _lib.AUGMENTED4
+
+
+@dataclass
+class DepthRescale:
+    """DepthRescale (segmenter.hpp:17-21): metric depth onto 0..255."""
+
+    min_mm: float = 0.0
+    max_mm: float = 4000.0
 
 
 class ModelBank:
@@ -241,9 +250,10 @@ class ModelBank:
     def __init__(self, width: int, height: int, mode, cfg: MixtureConfig, streams: int = 1,
                  device: int = 0, _borrowed=None):
         if isinstance(mode, str):
-            mode = {"Color3": _lib.COLOR3, "Depth1": _lib.DEPTH1}[mode]
+            mode = {"Color3": _lib.COLOR3, "Depth1": _lib.DEPTH1,
+                    "Augmented4": _lib.AUGMENTED4}[mode]
         self.width, self.height, self.streams, self.mode = width, height, streams, mode
-        self.channels = 3 if mode == _lib.COLOR3 else 1
+        self.channels = {_lib.COLOR3: 3, _lib.DEPTH1: 1, _lib.AUGMENTED4: 4}[mode]
         self.device = device
         self._owner = None
         if _borrowed is not None:
@@ -362,6 +372,23 @@ def segment_depth(bank: ModelBank, depth_mm, cfg: MixtureConfig, workers: int = 
     c = cfg._c()
     check(lib.rgbdseg_segment_depth(bank._h, _buf(d, np.uint16, bank.npx, "segment_depth"),
                                     C.byref(c), _buf(mask, np.uint8, bank.npx, "mask", True)))
+    return mask
+
+
+def segment_augmented(bank: ModelBank, r, g, b, depth_mm, rescale: DepthRescale,
+                      cfg: MixtureConfig, workers: int = 1, out=None):
+    """segment_augmented (segmenter.cpp:133-147) on the GPU."""
+    shp = bank._shape()
+    r, g, b = (_as_host(x, np.uint8, shp) for x in (r, g, b))
+    d = _as_host(depth_mm, np.uint16, shp)
+    mask, _ = _mask_out(out, bank.npx, shp)
+    c = cfg._c()
+    check(lib.rgbdseg_segment_augmented(
+        bank._h, _buf(r, np.uint8, bank.npx, "segment_augmented(r)"),
+        _buf(g, np.uint8, bank.npx, "segment_augmented(g)"),
+        _buf(b, np.uint8, bank.npx, "segment_augmented(b)"),
+        _buf(d, np.uint16, bank.npx, "segment_augmented(depth)"), float(rescale.min_mm),
+        float(rescale.max_mm), C.byref(c), _buf(mask, np.uint8, bank.npx, "mask", True)))
     return mask
 
 

@@ -473,7 +473,8 @@ def test_cpp_dropin_matches_reference_sequence_processor(cuda):
     exe = os.path.join(root, "integration", "_build", "dropin_test")
     if not os.path.exists(exe):
         pytest.skip("integration/_build/dropin_test not built (needs /root/reference)")
-    for args in (["40", "320", "240", "5"], ["12", "640", "480", "3"]):
+    for args in (["40", "320", "240", "5"], ["12", "640", "480", "3"],
+                 ["30", "256", "192", "4", "1"]):
         r = subprocess.run([exe, *args], capture_output=True, text=True, timeout=600)
         print(r.stdout)
         assert r.returncode == 0, r.stdout + r.stderr
@@ -566,3 +567,26 @@ def test_unregistered_processor_matches_oracle(R, port, streams):
             assert np.array_equal(sel(fm.fused).ravel(), fu), (f, s)
     with pytest.raises(ValueError, match="calibration"):
         R.SequenceProcessor(w, h, cfg, registered=False)
+
+
+def test_segment_augmented_matches_oracle(R, port):
+    """Augmented4 bank (segment_augmented, segmenter.cpp:133-147) on the GPU
+    vs the oracle (pinned to the reference), 2 streams, custom depth range."""
+    w, h, M, S = 80, 60, 5, 2
+    oc = O.color_cfg(M)
+    cfg = rcfg(R, oc)
+    bank = R.ModelBank(w, h, "Augmented4", cfg, streams=S)
+    ob = O.PortBank(port, S * w * h, 4, oc)
+    scenes = [O.PortScene(port, "B", w, h, seed=s + 3) for s in range(S)]
+    rs = R.DepthRescale(500.0, 3500.0)
+    for f in range(25):
+        frs = [sc.render(25 + f) for sc in scenes]
+        r, g, b = (np.stack([getattr(x, k) for x in frs]) for k in ("r", "g", "b"))
+        d = np.stack([holes(x.depth, f) for x in frs])
+        m = R.segment_augmented(bank, r, g, b, d, rs, cfg)
+        assert np.array_equal(m.ravel(), ob.segment_augmented(r, g, b, d, 500.0, 3500.0)), f
+    assert bank.planes().tobytes() == ob.planes().tobytes()
+    with pytest.raises(ValueError, match="range is empty"):
+        R.segment_augmented(bank, r, g, b, d, R.DepthRescale(10.0, 10.0), cfg)
+    with pytest.raises(ValueError, match="not Augmented4"):
+        R.segment_augmented(R.ModelBank(w, h, "Color3", cfg, streams=S), r, g, b, d, rs, cfg)

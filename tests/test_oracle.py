@@ -260,3 +260,36 @@ def test_port_unregistered_processor_matches_reference(port, ref):
         d = holes(fr.depth, f)
         for x, y in zip(pp.process(fr.r, fr.g, fr.b, d), rp.process(fr.r, fr.g, fr.b, d)):
             assert np.array_equal(x, y), f
+
+
+def _ref_bank_planes(ref, bank, M, Ch, n):
+    out = np.empty((M * Ch + 2 * M, n), np.float32)
+    k = 0
+    for i in range(M):
+        for c in range(Ch):
+            ref.check(ref.lib.rref_bank_get(bank, 0, i, c, out[k].ctypes.data))
+            k += 1
+    for kind in (1, 2):
+        for i in range(M):
+            ref.check(ref.lib.rref_bank_get(bank, kind, i, 0, out[k].ctypes.data))
+            k += 1
+    return out
+
+
+def test_port_augmented_matches_reference(port, ref):
+    """segment_augmented (segmenter.cpp:133-147), Augmented4 bank, against
+    the compiled reference: scenario A frames incl. depth 0 (no sentinel)."""
+    w, h, M = 64, 48, 4
+    cfg = O.color_cfg(M)
+    bank = ref.lib.rref_bank_create(w, h, 2, C.byref(cfg))
+    pb = O.PortBank(port, w * h, 4, cfg)
+    sc = O.PortScene(port, "A", w, h)
+    for f in range(30):
+        fr = sc.render(f)
+        d = holes(fr.depth, f)
+        rav = [np.ascontiguousarray(x).ravel() for x in (fr.r, fr.g, fr.b, d)]
+        mr = np.empty(w * h, np.uint8)
+        ref.check(ref.lib.rref_segment_augmented(bank, *rav, 0.0, 4000.0, C.byref(cfg), 1, mr))
+        assert np.array_equal(pb.segment_augmented(fr.r, fr.g, fr.b, d), mr), f
+    assert pb.planes().tobytes() == _ref_bank_planes(ref, bank, M, 4, w * h).tobytes()
+    ref.lib.rref_bank_destroy(bank)
