@@ -203,6 +203,18 @@ int rgbdseg_processor_submit(rgbdseg_processor* p, const uint8_t* r, const uint8
                              const uint8_t* b, const uint16_t* depth, uint8_t* fused_out,
                              uint8_t* rgb_out, uint8_t* depth_out);
 int rgbdseg_processor_sync(rgbdseg_processor* p);
+/* The same step plus the evaluation epilogue (confusion_counts,
+ * eval.cpp:11-31, fused into the kernel): gt = ground-truth mask planes
+ * (npx, {0,1}); counts receives int64 [streams][rgb, depth, fused][tp, fp,
+ * tn, fn] for this frame (host or device memory; valid after sync). */
+int rgbdseg_processor_process_eval(rgbdseg_processor* p, const uint8_t* r, const uint8_t* g,
+                                   const uint8_t* b, const uint16_t* depth, const uint8_t* gt,
+                                   int64_t* counts, uint8_t* fused_out, uint8_t* rgb_out,
+                                   uint8_t* depth_out);
+int rgbdseg_processor_submit_eval(rgbdseg_processor* p, const uint8_t* r, const uint8_t* g,
+                                  const uint8_t* b, const uint16_t* depth, const uint8_t* gt,
+                                  int64_t* counts, uint8_t* fused_out, uint8_t* rgb_out,
+                                  uint8_t* depth_out);
 int64_t rgbdseg_processor_frames(const rgbdseg_processor* p);
 /* Borrow the processor's banks / fusion state (owned by the processor):
  * color_bank()/depth_bank(), processor.hpp:67-68. */
@@ -216,6 +228,12 @@ void* rgbdseg_processor_stream(rgbdseg_processor* p);
  * 2 = write elision (words whose bits did not change are not rewritten).
  * Every variant produces the same bits; they differ only in HBM writes. */
 int rgbdseg_processor_set_variant(rgbdseg_processor* p, int variant);
+
+/* ---- evaluation: confusion_counts, eval.cpp:11-31 ------------------------
+ * pred/gt: npx mask bytes ({0,1}, host or device) split into `streams` equal
+ * frames; counts: int64 [streams][tp, fp, tn, fn].  Synchronous. */
+int rgbdseg_confusion_counts(const uint8_t* pred, const uint8_t* gt, size_t npx, int streams,
+                             int64_t* counts, int device);
 
 /* ---- synthetic scenes on the GPU (synthetic.cpp:119-195, harness) ------
  * Renders builtin scenario `name` ('A' or 'B'), frame `frame`, for `streams`

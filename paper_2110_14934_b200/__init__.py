@@ -16,8 +16,10 @@ from .rgbdseg import (  # noqa: F401
     RunConfig,
     SequenceProcessor,
     builtin_scenario_names,
+    confusion_counts,
     default_config_json,
     dilate_mask,
+    f1_score,
     fuse_step,
     init_mixture,
     init_mixtures,

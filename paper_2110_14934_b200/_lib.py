@@ -107,6 +107,9 @@ SIGNATURES = {
     "rgbdseg_processor_process": (_i, [_vp] * 8),
     "rgbdseg_processor_submit": (_i, [_vp] * 8),
     "rgbdseg_processor_sync": (_i, [_vp]),
+    "rgbdseg_processor_process_eval": (_i, [_vp] * 10),
+    "rgbdseg_processor_submit_eval": (_i, [_vp] * 10),
+    "rgbdseg_confusion_counts": (_i, [_vp, _vp, _sz, _i, _vp, _i]),
     "rgbdseg_processor_frames": (C.c_int64, [_vp]),
     "rgbdseg_processor_color_bank": (_vp, [_vp]),
     "rgbdseg_processor_depth_bank": (_vp, [_vp]),

@@ -175,7 +175,7 @@ struct rgbdseg_fusion {
 };
 
 struct Slot {
-    uint8_t *r = nullptr, *g = nullptr, *b = nullptr;
+    uint8_t *r = nullptr, *g = nullptr, *b = nullptr, *gt = nullptr;
     uint16_t* d = nullptr;
     uint8_t *rgbm = nullptr, *depm = nullptr;
     cudaEvent_t h2d_done = nullptr, k_done = nullptr, d2h_done = nullptr;
@@ -195,8 +195,9 @@ struct rgbdseg_processor {
     int64_t frames = 0;
     int variant = kAuto;
     // unregistered sequences: whole-frame scratch (inputs, masks, splat)
-    Scratch u_in, u_masks;
+    Scratch u_in, u_masks, u_gt;
     cudaEvent_t u_h2d = nullptr, u_k = nullptr;
+    Scratch counts;  // evaluation epilogue: [streams][3][4] uint64
 };
 
 extern "C" {
@@ -650,6 +651,7 @@ void rgbdseg_processor_destroy(rgbdseg_processor* p) {
         dfree(sl.d);
         dfree(sl.rgbm);
         dfree(sl.depm);
+        dfree(sl.gt);
         for (cudaEvent_t ev : {sl.h2d_done, sl.k_done, sl.d2h_done})
             if (ev) cudaEventDestroy(ev);
     }
@@ -730,6 +732,7 @@ static int ensure_slots(rgbdseg_processor* p) {
         if (!rc) rc = dalloc(&sl.d, p->chunk);
         if (!rc) rc = dalloc(&sl.rgbm, p->chunk);
         if (!rc) rc = dalloc(&sl.depm, p->chunk);
+        if (!rc) rc = dalloc(&sl.gt, p->chunk);
         if (rc) return rc;
     }
     return RGBDSEG_OK;
@@ -751,7 +754,8 @@ static FusedArgs base_args(const rgbdseg_processor* p) {
 // dilated, then List 1 fuses -- whole frames, in stream order.
 static int submit_unregistered(rgbdseg_processor* p, const uint8_t* r, const uint8_t* g,
                                const uint8_t* b, const uint16_t* depth, uint8_t* fused_out,
-                               uint8_t* rgb_out, uint8_t* depth_out) {
+                               uint8_t* rgb_out, uint8_t* depth_out, const uint8_t* gt,
+                               unsigned long long* dcounts) {
     const size_t n = p->npx;
     const int w = p->cfg.width, h = p->cfg.height, S = p->cfg.streams;
     void* ibuf;
@@ -798,6 +802,12 @@ static int submit_unregistered(rgbdseg_processor* p, const uint8_t* r, const uin
     uint8_t* fcopy = (fused_out && on_device(fused_out)) ? fused_out : nullptr;
     CU(launch_fuse(p->fusion->out, p->fusion->cpt, rgbm, reg, fcopy, p->cfg.fusion_counter_limit,
                    n, p->sc));
+    if (gt) {  // evaluation: the three masks against the ground truth
+        const void* dgt;
+        if (int rc = stage_in(gt, n, p->u_gt, &dgt, p->sc)) return rc;
+        const uint8_t* preds[3] = {rgbm, depm, p->fusion->out};
+        CU(launch_confusion(preds, 3, (const uint8_t*)dgt, n, (size_t)w * h, dcounts, p->sc));
+    }
     CU(cudaEventRecord(p->u_k, p->sc));
     CU(cudaStreamWaitEvent(p->sd2h, p->u_k, 0));
     if (fused_out && !fcopy) CU(cudaMemcpyAsync(fused_out, p->fusion->out, n, cudaMemcpyDefault, p->sd2h));
@@ -809,13 +819,26 @@ static int submit_unregistered(rgbdseg_processor* p, const uint8_t* r, const uin
     return RGBDSEG_OK;
 }
 
-int rgbdseg_processor_submit(rgbdseg_processor* p, const uint8_t* r, const uint8_t* g,
-                             const uint8_t* b, const uint16_t* depth, uint8_t* fused_out,
-                             uint8_t* rgb_out, uint8_t* depth_out) {
+static int submit_impl(rgbdseg_processor* p, const uint8_t* r, const uint8_t* g, const uint8_t* b,
+                       const uint16_t* depth, uint8_t* fused_out, uint8_t* rgb_out,
+                       uint8_t* depth_out, const uint8_t* gt, int64_t* counts_out) {
     if (!r || !g || !b || !depth) return fail(RGBDSEG_EINVAL, "process: null input plane");
-    GUARD(p->cfg.device);
-    if (!p->cfg.registered)
-        return submit_unregistered(p, r, g, b, depth, fused_out, rgb_out, depth_out);
+    if (gt && !counts_out) return fail(RGBDSEG_EINVAL, "process: ground truth without counts");
+    unsigned long long* dcounts = nullptr;
+    const size_t ncnt = (size_t)p->cfg.streams * 12;
+    if (gt) {
+        void* c;
+        if (int rc = p->counts.get(ncnt * sizeof(unsigned long long), &c)) return rc;
+        dcounts = static_cast<unsigned long long*>(c);
+        CU(cudaMemsetAsync(dcounts, 0, ncnt * sizeof(unsigned long long), p->sc));
+    }
+    const bool dgt = gt && on_device(gt);
+    if (!p->cfg.registered) {
+        int rc = submit_unregistered(p, r, g, b, depth, fused_out, rgb_out, depth_out, gt, dcounts);
+        if (!rc && gt)
+            CU(cudaMemcpyAsync(counts_out, dcounts, ncnt * 8, cudaMemcpyDefault, p->sd2h));
+        return rc;
+    }
     const bool dr = on_device(r), dg = on_device(g), db = on_device(b), dd = on_device(depth);
     const bool dfo = on_device(fused_out), dro = on_device(rgb_out), ddo = on_device(depth_out);
     const bool all_device = dr && dg && db && dd && (!fused_out || dfo) && (!rgb_out || dro) &&
@@ -823,7 +846,9 @@ int rgbdseg_processor_submit(rgbdseg_processor* p, const uint8_t* r, const uint8
     FusedArgs a = base_args(p);
     a.out = p->fusion->out;
     a.cpt = p->fusion->cpt;
-    if (all_device) {  // device-resident frames: one launch over every pixel
+    a.counts = dcounts;
+    a.stream_px = (size_t)p->cfg.width * p->cfg.height;
+    if (all_device && (!gt || dgt)) {  // device-resident frames: one launch over every pixel
         a.r = r;
         a.g = g;
         a.b = b;
@@ -833,9 +858,15 @@ int rgbdseg_processor_submit(rgbdseg_processor* p, const uint8_t* r, const uint8
         a.fused_copy = fused_out;
         a.base = 0;
         a.n = p->npx;
+        a.gt = gt;
         for (cudaEvent_t ev : p->chunk_d2h)  // a host-frame emit may still read out
             CU(cudaStreamWaitEvent(p->sc, ev, 0));
         CU(launch_fused(a, p->variant, p->sc));
+        if (gt) {
+            CU(cudaEventRecord(p->u_k, p->sc));
+            CU(cudaStreamWaitEvent(p->sd2h, p->u_k, 0));
+            CU(cudaMemcpyAsync(counts_out, dcounts, ncnt * 8, cudaMemcpyDefault, p->sd2h));
+        }
         ++p->frames;
         return RGBDSEG_OK;
     }
@@ -855,6 +886,8 @@ int rgbdseg_processor_submit(rgbdseg_processor* p, const uint8_t* r, const uint8
         if (!dg) CU(cudaMemcpyAsync(sl.g, g + lo, n, cudaMemcpyDefault, p->sh2d));
         if (!db) CU(cudaMemcpyAsync(sl.b, b + lo, n, cudaMemcpyDefault, p->sh2d));
         if (!dd) CU(cudaMemcpyAsync(sl.d, depth + lo, n * 2, cudaMemcpyDefault, p->sh2d));
+        a.gt = gt ? (dgt ? gt + lo : sl.gt) : nullptr;
+        if (gt && !dgt) CU(cudaMemcpyAsync(sl.gt, gt + lo, n, cudaMemcpyDefault, p->sh2d));
         CU(cudaEventRecord(sl.h2d_done, p->sh2d));
         // process: inputs landed, previous emit of this slot's masks and of
         // this chunk's fused labels finished
@@ -881,7 +914,53 @@ int rgbdseg_processor_submit(rgbdseg_processor* p, const uint8_t* r, const uint8
         CU(cudaEventRecord(sl.d2h_done, p->sd2h));
         CU(cudaEventRecord(p->chunk_d2h[c], p->sd2h));
     }
+    if (gt) CU(cudaMemcpyAsync(counts_out, dcounts, ncnt * 8, cudaMemcpyDefault, p->sd2h));
     ++p->frames;
+    return RGBDSEG_OK;
+}
+
+int rgbdseg_processor_submit(rgbdseg_processor* p, const uint8_t* r, const uint8_t* g,
+                             const uint8_t* b, const uint16_t* depth, uint8_t* fused_out,
+                             uint8_t* rgb_out, uint8_t* depth_out) {
+    GUARD(p->cfg.device);
+    return submit_impl(p, r, g, b, depth, fused_out, rgb_out, depth_out, nullptr, nullptr);
+}
+
+int rgbdseg_processor_submit_eval(rgbdseg_processor* p, const uint8_t* r, const uint8_t* g,
+                                  const uint8_t* b, const uint16_t* depth, const uint8_t* gt,
+                                  int64_t* counts, uint8_t* fused_out, uint8_t* rgb_out,
+                                  uint8_t* depth_out) {
+    GUARD(p->cfg.device);
+    return submit_impl(p, r, g, b, depth, fused_out, rgb_out, depth_out, gt, counts);
+}
+
+int rgbdseg_processor_process_eval(rgbdseg_processor* p, const uint8_t* r, const uint8_t* g,
+                                   const uint8_t* b, const uint16_t* depth, const uint8_t* gt,
+                                   int64_t* counts, uint8_t* fused_out, uint8_t* rgb_out,
+                                   uint8_t* depth_out) {
+    if (int rc = rgbdseg_processor_submit_eval(p, r, g, b, depth, gt, counts, fused_out, rgb_out,
+                                               depth_out))
+        return rc;
+    return rgbdseg_processor_sync(p);
+}
+
+int rgbdseg_confusion_counts(const uint8_t* pred, const uint8_t* gt, size_t npx, int streams,
+                             int64_t* counts, int device) {
+    if (streams <= 0 || npx % (size_t)streams != 0)
+        return fail(RGBDSEG_EINVAL, "confusion_counts: pixels do not split into streams");
+    GUARD(device);
+    Scratch sp, sg, sc;
+    const void *dp, *dg;
+    if (int rc = stage_in(pred, npx, sp, &dp, 0)) return rc;
+    if (int rc = stage_in(gt, npx, sg, &dg, 0)) return rc;
+    void* c;
+    if (int rc = sc.get((size_t)streams * 4 * 8, &c)) return rc;
+    CU(cudaMemsetAsync(c, 0, (size_t)streams * 4 * 8, 0));
+    const uint8_t* preds[1] = {(const uint8_t*)dp};
+    CU(launch_confusion(preds, 1, (const uint8_t*)dg, npx, npx / streams,
+                        static_cast<unsigned long long*>(c), 0));
+    CU(cudaMemcpyAsync(counts, c, (size_t)streams * 4 * 8, cudaMemcpyDefault, 0));
+    CU(cudaStreamSynchronize(0));
     return RGBDSEG_OK;
 }
 

@@ -122,15 +122,90 @@ __device__ __forceinline__ uint32_t bank_pixel(Mixture<M, C>& m, const float* sr
     return label;
 }
 
+// ---------------------------------------------------------------- evaluation
+// Per-stream confusion counts of up to 3 methods in one block: each warp
+// popcounts ballots, warps add into shared slots for the (at most two)
+// streams a 256-pixel block can touch when streams hold >= 256 pixels, and
+// one thread per nonzero counter adds it to the global int64 counters; a
+// warp whose pixels fall in another stream adds directly.  tn is derived
+// from the counted pixels: eval.cpp:17-28 assigns every pixel exactly one.
+template <int NM>
+__device__ __forceinline__ void eval_accumulate(bool active, size_t j, size_t stream_px,
+                                                const uint32_t (&pred)[NM], uint32_t gt,
+                                                unsigned long long* counts) {
+    __shared__ unsigned int part[2][NM][4];
+    __shared__ unsigned long long s0;
+    const int tid = threadIdx.x;
+    const unsigned lane = tid & 31;
+    const size_t s = active ? j / stream_px : ~size_t(0);
+    if (tid < 2 * NM * 4) (&part[0][0][0])[tid] = 0u;
+    if (tid == 0) s0 = s;  // thread 0 of a launched block is always active
+    __syncthreads();
+    const size_t base_s = s0;
+    const size_t s_lane0 = __shfl_sync(0xffffffffu, s, 0);
+    const bool uniform = __all_sync(0xffffffffu, !active || s == s_lane0);
+    if (uniform) {
+        const unsigned act = __ballot_sync(0xffffffffu, active);
+#pragma unroll
+        for (int m = 0; m < NM; ++m) {
+            const unsigned p1 = __ballot_sync(0xffffffffu, active && pred[m]);
+            const unsigned g1 = __ballot_sync(0xffffffffu, active && gt);
+            const unsigned tp = __popc(p1 & g1), fp = __popc(p1 & ~g1), fn = __popc(~p1 & g1 & act);
+            const unsigned tn = __popc(act) - tp - fp - fn;
+            if (lane == 0 && act) {
+                const size_t slot = s_lane0 - base_s;
+                if (slot < 2) {
+                    atomicAdd(&part[slot][m][0], tp);
+                    atomicAdd(&part[slot][m][1], fp);
+                    atomicAdd(&part[slot][m][2], tn);
+                    atomicAdd(&part[slot][m][3], fn);
+                } else {
+                    unsigned long long* c = counts + (s_lane0 * NM + m) * 4;
+                    atomicAdd(c + 0, (unsigned long long)tp);
+                    atomicAdd(c + 1, (unsigned long long)fp);
+                    atomicAdd(c + 2, (unsigned long long)tn);
+                    atomicAdd(c + 3, (unsigned long long)fn);
+                }
+            }
+        }
+    } else if (active) {  // tiny streams: per-pixel atomics
+#pragma unroll
+        for (int m = 0; m < NM; ++m) {
+            const int k = pred[m] ? (gt ? 0 : 1) : (gt ? 3 : 2);
+            atomicAdd(counts + (s * NM + m) * 4 + k, 1ull);
+        }
+    }
+    __syncthreads();
+    if (tid < 2 * NM * 4) {
+        const unsigned v = (&part[0][0][0])[tid];
+        const int slot = tid / (NM * 4);
+        if (v) atomicAdd(counts + (base_s + slot) * NM * 4 + (tid % (NM * 4)), (unsigned long long)v);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads)
+    k_confusion(const uint8_t* __restrict__ p0, const uint8_t* __restrict__ p1,
+                const uint8_t* __restrict__ p2, int methods, const uint8_t* __restrict__ gt,
+                size_t n, size_t stream_px, unsigned long long* counts) {
+    const size_t j = (size_t)blockIdx.x * kThreads + threadIdx.x;
+    const bool active = j < n;
+    const uint32_t g = active ? gt[j] : 0u;
+    if (methods == 1) {
+        const uint32_t pr[1] = {active ? p0[j] : 0u};
+        eval_accumulate<1>(active, j, stream_px, pr, g, counts);
+    } else {
+        const uint32_t pr[3] = {active ? p0[j] : 0u, active ? p1[j] : 0u, active ? p2[j] : 0u};
+        eval_accumulate<3>(active, j, stream_px, pr, g, counts);
+    }
+}
+
 // ---------------------------------------------------------------- K1 fused
-template <int MC, int MD, bool kElide>
 #ifndef RGBDSEG_FUSED_MIN_BLOCKS
 #define RGBDSEG_FUSED_MIN_BLOCKS 3
 #endif
-__global__ void __launch_bounds__(kThreads, RGBDSEG_FUSED_MIN_BLOCKS)
-    k_fused_ldg(const __grid_constant__ FusedArgs a) {
-    const size_t i = (size_t)blockIdx.x * kThreads + threadIdx.x;
-    if (i >= a.n) return;
+// One pixel of K1; returns the three labels for the evaluation epilogue.
+template <int MC, int MD, bool kElide>
+__device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i, uint32_t (&lab)[3]) {
     const size_t j = a.base + i;
 
     // Issue every load of the pixel before any math: inputs, flags, fusion
@@ -190,6 +265,22 @@ __global__ void __launch_bounds__(kThreads, RGBDSEG_FUSED_MIN_BLOCKS)
     if (a.rgb_mask) st_stream(a.rgb_mask + i, (uint8_t)lc);
     if (a.depth_mask) st_stream(a.depth_mask + i, (uint8_t)ld);
     if (a.fused_copy) st_stream(a.fused_copy + i, (uint8_t)out);
+    lab[0] = lc;
+    lab[1] = ld;
+    lab[2] = out;
+}
+
+template <int MC, int MD, bool kElide>
+__global__ void __launch_bounds__(kThreads, RGBDSEG_FUSED_MIN_BLOCKS)
+    k_fused_ldg(const __grid_constant__ FusedArgs a) {
+    const size_t i = (size_t)blockIdx.x * kThreads + threadIdx.x;
+    const bool active = i < a.n;
+    uint32_t lab[3] = {0u, 0u, 0u};
+    if (active) fused_pixel<MC, MD, kElide>(a, i, lab);
+    if (a.gt) {  // evaluation epilogue: the masks never leave registers
+        const uint32_t g = active ? (uint32_t)ld_stream(a.gt + i) : 0u;
+        eval_accumulate<3>(active, a.base + i, a.stream_px, lab, g, a.counts);
+    }
 }
 
 // ---------------------------------------------------------------- K1b banks
@@ -669,6 +760,14 @@ cudaError_t launch_dilate(const uint8_t* in, uint8_t* tmp, uint8_t* out, int w, 
     cudaError_t e = go(k_dilate_pass<true>, n, s, in, tmp, w, h, n, radius);
     if (e != cudaSuccess) return e;
     return go(k_dilate_pass<false>, n, s, (const uint8_t*)tmp, out, w, h, n, radius);
+}
+
+cudaError_t launch_confusion(const uint8_t* const* preds, int methods, const uint8_t* gt,
+                             size_t npx, size_t stream_px, unsigned long long* counts,
+                             cudaStream_t s) {
+    if (methods != 1 && methods != 3) return cudaErrorInvalidValue;
+    return go(k_confusion, npx, s, preds[0], methods == 3 ? preds[1] : preds[0],
+              methods == 3 ? preds[2] : preds[0], methods, gt, npx, stream_px, counts);
 }
 
 uint64_t launches() { return g_launches.load(); }

@@ -54,6 +54,13 @@ struct FusedArgs {
     MixCfg dk;
     int limit;
     int fuse;  // 0: unregistered sequence -- write rgb/depth masks, fuse after registration
+    // optional evaluation epilogue (confusion_counts, eval.cpp:11-31): ground
+    // truth for pixels [0, n) and per-stream int64 counters
+    // [stream][method rgb, depth, fused][tp, fp, tn, fn]; stream of pixel
+    // base+i is (base+i) / stream_px.
+    const uint8_t* gt;
+    unsigned long long* counts;
+    size_t stream_px;
 };
 
 // Kernel variants of K1 (identical results; they differ in HBM writes).
@@ -132,6 +139,12 @@ cudaError_t launch_register_splat(const uint8_t* mask, const uint16_t* depth, in
 // the reference's border clipping).  tmp: scratch of the same size.
 cudaError_t launch_dilate(const uint8_t* in, uint8_t* tmp, uint8_t* out, int w, int h,
                           int streams, int radius, cudaStream_t s);
+
+// confusion_counts (eval.cpp:11-31) of `methods` prediction planes against gt
+// over npx pixels, accumulated into counts[stream][method][tp, fp, tn, fn].
+cudaError_t launch_confusion(const uint8_t* const* preds, int methods, const uint8_t* gt,
+                             size_t npx, size_t stream_px, unsigned long long* counts,
+                             cudaStream_t s);
 
 uint64_t launches();
 

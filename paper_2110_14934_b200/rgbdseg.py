@@ -530,12 +530,15 @@ def dilate_mask(mask, radius: int, device: int = 0):
 
 @dataclass
 class FrameMasks:
-    """FrameMasks (processor.hpp:46-53) for the fused method."""
+    """FrameMasks (processor.hpp:46-53) for the fused method.  `counts`
+    (with ground truth): int64 [streams, 3 (rgb, depth, fused), 4 (tp, fp,
+    tn, fn)] from the kernel's evaluation epilogue."""
 
     index: int
     rgb: Optional[object] = None
     depth: Optional[object] = None
     fused: Optional[object] = None
+    counts: Optional[np.ndarray] = None
 
 
 class SequenceProcessor:
@@ -619,9 +622,12 @@ class SequenceProcessor:
                 _buf(dep, np.uint8, n, "depth_mask", True)]
         return ptrs, (r, g, b, depth)
 
-    def process(self, r, g, b, depth, want=("rgb", "depth", "fused"), out=None) -> FrameMasks:
+    def process(self, r, g, b, depth, want=("rgb", "depth", "fused"), out=None,
+                gt=None) -> FrameMasks:
         """SequenceProcessor::process (processor.cpp:158-184), synchronous.
-        `out` may map 'rgb'/'depth'/'fused' to preallocated arrays/tensors."""
+        `out` may map 'rgb'/'depth'/'fused' to preallocated arrays/tensors.
+        With `gt` (ground-truth masks) the kernel also returns the frame's
+        confusion counts (eval.cpp:11-31) without the masks leaving the GPU."""
         out = dict(out or {})
         shp = self._shape()
         for k in want:
@@ -629,8 +635,16 @@ class SequenceProcessor:
                 out[k] = np.empty(shp, np.uint8)
         ptrs, keep = self._args(r, g, b, depth, out.get("fused"), out.get("rgb"), out.get("depth"))
         idx = self.frames
-        check(lib.rgbdseg_processor_process(self._h, *ptrs), "process")
-        return FrameMasks(idx, out.get("rgb"), out.get("depth"), out.get("fused"))
+        if gt is None:
+            check(lib.rgbdseg_processor_process(self._h, *ptrs), "process")
+            return FrameMasks(idx, out.get("rgb"), out.get("depth"), out.get("fused"))
+        gt = _as_host(gt, np.uint8, shp)
+        _check_mask(gt)
+        counts = np.zeros((self.streams, 3, 4), np.int64)
+        check(lib.rgbdseg_processor_process_eval(self._h, *ptrs[:4],
+                                                 _buf(gt, np.uint8, self.npx, "gt"),
+                                                 counts.ctypes.data, *ptrs[4:]), "process")
+        return FrameMasks(idx, out.get("rgb"), out.get("depth"), out.get("fused"), counts)
 
     def submit(self, r, g, b, depth, fused=None, rgb=None, depth_mask=None):
         """Enqueue one step without waiting; buffers must stay alive and
@@ -642,6 +656,38 @@ class SequenceProcessor:
     def sync(self):
         check(lib.rgbdseg_processor_sync(self._h), "sync")
         self._keep.clear()
+
+
+# ------------------------------------------------------------------ evaluation
+
+def confusion_counts(pred, gt, streams: int = 1, device: int = 0):
+    """confusion_counts (eval.cpp:11-31; module.cpp:112-116) on the GPU:
+    (tp, fp, tn, fn), or an int64 [streams, 4] array when streams > 1."""
+    _check_mask(pred)
+    _check_mask(gt)
+    p = _as_host(pred, np.uint8, np.shape(pred))
+    g = _as_host(gt, np.uint8, np.shape(pred))
+    n = int(np.prod(np.shape(pred)))
+    counts = np.zeros((streams, 4), np.int64)
+    check(lib.rgbdseg_confusion_counts(_buf(p, np.uint8, n, "pred"), _buf(g, np.uint8, n, "gt"),
+                                       n, streams, counts.ctypes.data, device))
+    return tuple(int(x) for x in counts[0]) if streams == 1 else counts
+
+
+def precision(tp, fp):
+    """eval.cpp:33-37: TP / (TP + FP), 0 when the denominator is 0."""
+    return tp / (tp + fp) if tp + fp > 0 else 0.0
+
+
+def recall(tp, fn):
+    """eval.cpp:39-43: TP / (TP + FN), 0 when the denominator is 0."""
+    return tp / (tp + fn) if tp + fn > 0 else 0.0
+
+
+def f1_score(tp, fp, fn):
+    """f1 (eval.cpp:45-47; module.cpp:117-119): 2PR / (P + R), 0 if P + R = 0."""
+    p, r = precision(tp, fp), recall(tp, fn)
+    return 2.0 * p * r / (p + r) if p + r > 0.0 else 0.0
 
 
 # ------------------------------------------------------------------ scenes
