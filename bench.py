@@ -448,6 +448,7 @@ def main():
                          "traffic": round(traffic) if traffic is not None else None,
                          "achieved_basis": basis, "peak_source": peak_src,
                          "kernel_ms": round(launch_ms, 4),
+                         "kernel_ms_min_max": [round(min(kernel_ms), 4), round(max(kernel_ms), 4)],
                          "dense_algorithmic_bytes_per_px": bpp,
                          "dense_equivalent_gbs": round(dense_gbs, 1),
                          "dense_equivalent_frac": round(dense_gbs / peak, 4)},

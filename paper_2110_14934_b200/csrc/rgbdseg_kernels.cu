@@ -145,37 +145,62 @@ __device__ __forceinline__ uint32_t bank_step_lazy(float* px, const float (&v)[C
             rank[j] += j_first ? 0 : 1;
         }
 
-    // ---- match: probe means in ranked order --------------------------------
-    int matched = -1, mrank = M;
-    float mu[C], vm = 0.0f;
-#pragma unroll
-    for (int c = 0; c < C; ++c) mu[c] = 0.0f;
+    // ---- match: probe means in ranked order, at most two round trips ------
+    // Round 1 reads the first-ranked component's mean; only if it misses are
+    // the remaining components' means read, all at once (an unmatched pixel
+    // -- 0.7% of colour pixel-frames, but most of a frame during an
+    // illumination step -- would otherwise chain M dependent loads).
+    int ord[M];
+    float ordsd[M], ordvar[M];
 #pragma unroll
     for (int r = 0; r < M; ++r) {
-        if (matched < 0) {
-            int i = 0;
-            float si = 0.0f, vi = 0.0f;
+        ord[r] = 0;
+        ordsd[r] = 0.0f;
+        ordvar[r] = 0.0f;
 #pragma unroll
-            for (int q = 0; q < M; ++q)
-                if (rank[q] == r) {
-                    i = q;
-                    si = sd[q];
-                    vi = var[q];
-                }
-            const float band = fmul(k.lambda, si);
-            float m[C];
-            bool in = true;
-#pragma unroll
-            for (int c = 0; c < C; ++c) {
-                m[c] = ld_stream(px + (i * C + c) * kBlockPx);
-                in = in && (fabsf(fsub(v[c], m[c])) < band);
+        for (int q = 0; q < M; ++q)
+            if (rank[q] == r) {
+                ord[r] = q;
+                ordsd[r] = sd[q];
+                ordvar[r] = var[q];
             }
-            if (in) {
-                matched = i;
-                mrank = r;
-                vm = vi;
+    }
+    int matched = -1, mrank = M;
+    float mu[C], vm = 0.0f;
+    {
+        bool in = true;
+        const float band = fmul(k.lambda, ordsd[0]);
 #pragma unroll
-                for (int c = 0; c < C; ++c) mu[c] = m[c];
+        for (int c = 0; c < C; ++c) {
+            mu[c] = ld_stream(px + (ord[0] * C + c) * kBlockPx);
+            in = in && (fabsf(fsub(v[c], mu[c])) < band);
+        }
+        if (in) {
+            matched = ord[0];
+            mrank = 0;
+            vm = ordvar[0];
+        }
+    }
+    if (matched < 0) {
+        float m[M - 1][C];
+#pragma unroll
+        for (int r = 1; r < M; ++r)
+#pragma unroll
+            for (int c = 0; c < C; ++c) m[r - 1][c] = ld_stream(px + (ord[r] * C + c) * kBlockPx);
+#pragma unroll
+        for (int r = 1; r < M; ++r) {
+            if (matched < 0) {
+                const float band = fmul(k.lambda, ordsd[r]);
+                bool in = true;
+#pragma unroll
+                for (int c = 0; c < C; ++c) in = in && (fabsf(fsub(v[c], m[r - 1][c])) < band);
+                if (in) {
+                    matched = ord[r];
+                    mrank = r;
+                    vm = ordvar[r];
+#pragma unroll
+                    for (int c = 0; c < C; ++c) mu[c] = m[r - 1][c];
+                }
             }
         }
     }
