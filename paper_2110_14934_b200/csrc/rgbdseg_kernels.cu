@@ -78,6 +78,27 @@ __device__ __forceinline__ void store_mix(float* s, const Mixture<M, C>& m) {
     for (int i = 0; i < M; ++i) st_stream(s + (M * C + M + i) * kBlockPx, m.w[i]);
 }
 
+// Elided store: identical memory image to store_mix, but words whose bits
+// did not change are not rewritten.  Only the matched / replaced component's
+// mean and variance can change in a step (mixture.cpp:105-113, 125-128); the
+// weights are compared individually.  touched < 0 means "all" (init).
+template <int M, int C>
+__device__ __forceinline__ void store_mix_elide(float* s, const Mixture<M, C>& m, int touched,
+                                                const float (&w_old)[M]) {
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        if (touched < 0 || touched == i) {
+#pragma unroll
+            for (int c = 0; c < C; ++c) st_stream(s + (i * C + c) * kBlockPx, m.mu[i][c]);
+            st_stream(s + (M * C + i) * kBlockPx, m.var[i]);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < M; ++i)
+        if (touched < 0 || __float_as_uint(m.w[i]) != __float_as_uint(w_old[i]))
+            st_stream(s + (M * C + M + i) * kBlockPx, m.w[i]);
+}
+
 // run_bank's per-pixel body (segmenter.cpp:80-96) on a mixture loaded from
 // `src`.  The branch-free fast step runs first; a pixel whose operands leave
 // its exact ranges (gmm_pixel.cuh) is reloaded and replayed by the generic
@@ -99,248 +120,6 @@ __device__ __forceinline__ uint32_t bank_pixel(Mixture<M, C>& m, const float* sr
         label = gmm_step(m, v, k, touched);
     }
     return label;
-}
-
-// ---------------------------------------------------------------- lazy bank step
-// The elided K1 step for one tiled bank.  Only the weights and variances are
-// read up front; means are fetched in ranked order until the first component
-// whose band contains the observation (match_component, mixture.cpp:74-92),
-// which on a settled background is the first one probed: the other
-// components' means are never read.  The update touches one component
-// (mixture.cpp:105-113 or 125-128), so its mean and variance are stored at a
-// dynamic plane offset and only the weights whose bits changed are
-// rewritten.  Same fast arithmetic and preconditions as gmm_step_fast; ok ==
-// false means the caller replays the pixel with the generic step.
-template <int M, int C>
-__device__ __forceinline__ uint32_t bank_step_lazy(float* px, const float (&v)[C], const MixCfg& k,
-                                                   const float (&w0)[M], const float (&var)[M],
-                                                   bool& ok) {
-    uint32_t vmin = __float_as_uint(var[0]), vmax = vmin;
-    uint32_t wmax = __float_as_uint(w0[0]), wnz = wmax - 1u;
-#pragma unroll
-    for (int i = 1; i < M; ++i) {
-        const uint32_t vb = __float_as_uint(var[i]), wb = __float_as_uint(w0[i]);
-        vmin = min(vmin, vb);
-        vmax = max(vmax, vb);
-        wmax = max(wmax, wb);
-        wnz = min(wnz, wb - 1u);
-    }
-    ok = ok && vmin >= kVarLo && vmax < kVarHi && wmax < kBitsHi && wnz >= kBitsLo - 1u;
-
-    float sd[M], fit[M];
-#pragma unroll
-    for (int i = 0; i < M; ++i) {
-        sd[i] = fsqrt_seq(var[i]);
-        fit[i] = fdiv_seq(w0[i], sd[i]);
-    }
-    int rank[M];
-#pragma unroll
-    for (int i = 0; i < M; ++i) rank[i] = 0;
-#pragma unroll
-    for (int i = 0; i < M; ++i)
-#pragma unroll
-        for (int j = i + 1; j < M; ++j) {
-            const bool j_first = fit[j] > fit[i];
-            rank[i] += j_first ? 1 : 0;
-            rank[j] += j_first ? 0 : 1;
-        }
-
-    // ---- match: probe means in ranked order, at most two round trips ------
-    // Round 1 reads the first-ranked component's mean; only if it misses are
-    // the remaining components' means read, all at once (an unmatched pixel
-    // -- 0.7% of colour pixel-frames, but most of a frame during an
-    // illumination step -- would otherwise chain M dependent loads).
-    int ord[M];
-    float ordsd[M], ordvar[M];
-#pragma unroll
-    for (int r = 0; r < M; ++r) {
-        ord[r] = 0;
-        ordsd[r] = 0.0f;
-        ordvar[r] = 0.0f;
-#pragma unroll
-        for (int q = 0; q < M; ++q)
-            if (rank[q] == r) {
-                ord[r] = q;
-                ordsd[r] = sd[q];
-                ordvar[r] = var[q];
-            }
-    }
-    int matched = -1, mrank = M;
-    float mu[C], vm = 0.0f;
-    {
-        bool in = true;
-        const float band = fmul(k.lambda, ordsd[0]);
-#pragma unroll
-        for (int c = 0; c < C; ++c) {
-            mu[c] = ld_stream(px + (ord[0] * C + c) * kBlockPx);
-            in = in && (fabsf(fsub(v[c], mu[c])) < band);
-        }
-        if (in) {
-            matched = ord[0];
-            mrank = 0;
-            vm = ordvar[0];
-        }
-    }
-    if (matched < 0) {
-        float m[M - 1][C];
-#pragma unroll
-        for (int r = 1; r < M; ++r)
-#pragma unroll
-            for (int c = 0; c < C; ++c) m[r - 1][c] = ld_stream(px + (ord[r] * C + c) * kBlockPx);
-#pragma unroll
-        for (int r = 1; r < M; ++r) {
-            if (matched < 0) {
-                const float band = fmul(k.lambda, ordsd[r]);
-                bool in = true;
-#pragma unroll
-                for (int c = 0; c < C; ++c) in = in && (fabsf(fsub(v[c], m[r - 1][c])) < band);
-                if (in) {
-                    matched = ord[r];
-                    mrank = r;
-                    vm = ordvar[r];
-#pragma unroll
-                    for (int c = 0; c < C; ++c) mu[c] = m[r - 1][c];
-                }
-            }
-        }
-    }
-
-    // ---- classify (mixture.cpp:133-146) ------------------------------------
-    uint32_t label = 1u;
-    if (matched >= 0) {
-        if (mrank == 0) {
-            label = 0u;
-        } else {
-            float cum = 0.0f;
-            bool done = false;
-#pragma unroll
-            for (int r = 0; r < M; ++r) {
-                if (!done) {
-                    float wr = 0.0f;
-#pragma unroll
-                    for (int i = 0; i < M; ++i)
-                        if (rank[i] == r) wr = w0[i];
-                    cum = fadd(cum, wr);
-                    if (r == mrank) {
-                        label = 0u;
-                        done = true;
-                    } else if (cum > k.T) {
-                        done = true;
-                    }
-                }
-            }
-        }
-    }
-
-    // ---- update (mixture.cpp:94-131) ---------------------------------------
-    const float a = k.alpha;
-    float w[M];
-    int t;
-    float vt;
-    if (matched >= 0) {
-        const float oma = fsub(1.0f, a);
-#pragma unroll
-        for (int i = 0; i < M; ++i) w[i] = fadd(fmul(oma, w0[i]), (i == matched) ? a : 0.0f);
-        float sum = 0.0f;
-#pragma unroll
-        for (int i = 0; i < M; ++i) sum = fadd(sum, w[i]);
-        if (sum > 0.0f) {
-            ok = ok && pos_in_range(sum);
-            const float inv = fdiv_seq(1.0f, sum);
-#pragma unroll
-            for (int i = 0; i < M; ++i) w[i] = fmul(w[i], inv);
-        }
-        float wm = w[0];
-#pragma unroll
-        for (int i = 1; i < M; ++i)
-            if (i == matched) wm = w[i];
-        const float den = stdmax(wm, a);
-        ok = ok && pos_in_range(den);
-        const float rho = fdiv_seq(a, den);
-        const float omr = fsub(1.0f, rho);
-        float d2 = 0.0f;
-#pragma unroll
-        for (int c = 0; c < C; ++c) {
-            mu[c] = fadd(fmul(omr, mu[c]), fmul(rho, v[c]));
-            const float d = fsub(v[c], mu[c]);
-            d2 = fadd(d2, fmul(d, d));
-        }
-        const float rd = fmul(rho, d2);
-        float q = rd;
-        if (C != 1) {
-            ok = ok && zero_or_in_range(rd);
-            q = fdiv_seq(rd, (float)C);
-        }
-        vt = stdmax(fadd(fmul(omr, vm), q), k.var_floor);
-        t = matched;
-    } else {
-        int weakest = 0;
-        float worst = fit[0];
-#pragma unroll
-        for (int i = 1; i < M; ++i)
-            if (fit[i] < worst) {
-                worst = fit[i];
-                weakest = i;
-            }
-#pragma unroll
-        for (int i = 0; i < M; ++i) w[i] = (i == weakest) ? k.w_new : w0[i];
-        float sum = 0.0f;
-#pragma unroll
-        for (int i = 0; i < M; ++i) sum = fadd(sum, w[i]);
-        if (sum > 0.0f) {
-            ok = ok && pos_in_range(sum);
-            const float inv = fdiv_seq(1.0f, sum);
-#pragma unroll
-            for (int i = 0; i < M; ++i) w[i] = fmul(w[i], inv);
-        }
-#pragma unroll
-        for (int c = 0; c < C; ++c) mu[c] = v[c];
-        vt = fmul(k.sigma0, k.sigma0);
-        t = weakest;
-    }
-    if (ok) {  // elided write-back: the touched component + changed weights
-#pragma unroll
-        for (int c = 0; c < C; ++c) st_stream(px + (t * C + c) * kBlockPx, mu[c]);
-        st_stream(px + (M * C + t) * kBlockPx, vt);
-#pragma unroll
-        for (int i = 0; i < M; ++i)
-            if (__float_as_uint(w[i]) != __float_as_uint(w0[i]))
-                st_stream(px + (M * C + M + i) * kBlockPx, w[i]);
-    }
-    return label;
-}
-
-// One bank of one pixel for the elided K1: init, lazy fast step, or the
-// exact replay (full reload, generic step, dense store).
-template <int M, int C>
-__device__ __forceinline__ uint32_t bank_pixel_lazy(float* px, uint8_t* flag, bool initialised,
-                                                    const float (&v)[C], const MixCfg& k,
-                                                    const float (&w0)[M], const float (&var)[M]) {
-    if (!initialised) {
-        Mixture<M, C> m;
-        gmm_init(m, v, k);
-        store_mix(px, m);
-        st_stream(flag, (uint8_t)1);
-        return 0u;
-    }
-    bool ok = k.fast != 0;
-    uint32_t label = bank_step_lazy<M, C>(px, v, k, w0, var, ok);
-    if (!ok) {
-        Mixture<M, C> m;
-        load_mix(px, m);
-        int t;
-        label = gmm_step(m, v, k, t);
-        store_mix(px, m);
-    }
-    return label;
-}
-
-template <int M, int C>
-__device__ __forceinline__ void load_wv(const float* px, float (&w)[M], float (&var)[M]) {
-#pragma unroll
-    for (int i = 0; i < M; ++i) var[i] = ld_stream(px + (M * C + i) * kBlockPx);
-#pragma unroll
-    for (int i = 0; i < M; ++i) w[i] = ld_stream(px + (M * C + M + i) * kBlockPx);
 }
 
 // ---------------------------------------------------------------- evaluation
@@ -429,9 +208,8 @@ template <int MC, int MD, bool kElide>
 __device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i, uint32_t (&lab)[3]) {
     const size_t j = a.base + i;
 
-    // Issue the pixel's loads before any math: inputs, flags, fusion state and
-    // the mixtures (dense: all 40 words at M=5/5; elided: weights and
-    // variances, the means follow on demand in ranked order).
+    // Issue every load of the pixel before any math: inputs, flags, fusion
+    // state and both mixtures (40 planes at M=5) are independent requests.
     const float vc[3] = {(float)ld_stream(a.r + i), (float)ld_stream(a.g + i),
                          (float)ld_stream(a.b + i)};
     const uint32_t raw = ld_stream(a.d + i);
@@ -443,33 +221,37 @@ __device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i, uint32
     const bool dinit = ld_stream(dfl) != 0;
     const uint32_t out0 = a.fuse ? ld_stream(a.out + i) : 0u;
     const int cpt0 = a.fuse ? (int)ld_stream(a.cpt + i) : 0;
-    uint32_t lc = 0, ld = 0;
-    if (kElide) {
-        // weights + variances of both banks first; means on demand
-        float cw[MC], cv[MC], dw[MD], dv[MD];
-        load_wv<MC, 3>(cs, cw, cv);
-        load_wv<MD, 1>(ds, dw, dv);
-        lc = bank_pixel_lazy<MC, 3>(cs, cfl, cinit, vc, a.ck, cw, cv);
-        if (raw != 0) {  // segment_depth: raw 0 = no return
-            const float vd[1] = {(float)raw};
-            ld = bank_pixel_lazy<MD, 1>(ds, dfl, dinit, vd, a.dk, dw, dv);
-        }
-    } else {
-        Mixture<MC, 3> cm;
-        Mixture<MD, 1> dm;
-        load_mix(cs, cm);
-        load_mix(ds, dm);
-        int ct = 0;
-        lc = bank_pixel(cm, cs, vc, cinit, a.ck, ct);
+    Mixture<MC, 3> cm;
+    Mixture<MD, 1> dm;
+    load_mix(cs, cm);
+    load_mix(ds, dm);
+
+    // ---- colour stream (segment_color) ----
+    float cw_old[MC];
+#pragma unroll
+    for (int q = 0; q < MC; ++q) cw_old[q] = cm.w[q];
+    int ct = 0;
+    const uint32_t lc = bank_pixel(cm, cs, vc, cinit, a.ck, ct);
+    if (kElide)
+        store_mix_elide(cs, cm, ct, cw_old);
+    else
         store_mix(cs, cm);
-        if (!cinit) st_stream(cfl, (uint8_t)1);
-        if (raw != 0) {
-            const float vd[1] = {(float)raw};
-            int dt = 0;
-            ld = bank_pixel(dm, ds, vd, dinit, a.dk, dt);
+    if (!cinit) st_stream(cfl, (uint8_t)1);
+
+    // ---- depth stream (segment_depth): raw 0 = no return ----
+    uint32_t ld = 0;
+    if (raw != 0) {
+        const float vd[1] = {(float)raw};
+        float dw_old[MD];
+#pragma unroll
+        for (int q = 0; q < MD; ++q) dw_old[q] = dm.w[q];
+        int dt = 0;
+        ld = bank_pixel(dm, ds, vd, dinit, a.dk, dt);
+        if (kElide)
+            store_mix_elide(ds, dm, dt, dw_old);
+        else
             store_mix(ds, dm);
-            if (!dinit) st_stream(dfl, (uint8_t)1);
-        }
+        if (!dinit) st_stream(dfl, (uint8_t)1);
     }
 
     // ---- List-1 fusion on the registered depth mask ----
