@@ -200,8 +200,11 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // ---------------------------------------------------------------- K1 fused
+// Resident blocks per SM: the dense variant is HBM-bound at 3 (80 regs);
+// the elided one is latency-bound and gains from 4 (64 regs, 32 warps/SM)
+// despite a few spilled words (profiles/variants_r01.json).
 #ifndef RGBDSEG_FUSED_MIN_BLOCKS
-#define RGBDSEG_FUSED_MIN_BLOCKS 3
+#define RGBDSEG_FUSED_MIN_BLOCKS(elide) ((elide) ? 4 : 3)
 #endif
 // One pixel of K1; returns the three labels for the evaluation epilogue.
 template <int MC, int MD, bool kElide>
@@ -271,7 +274,7 @@ __device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i, uint32
 }
 
 template <int MC, int MD, bool kElide>
-__global__ void __launch_bounds__(kThreads, RGBDSEG_FUSED_MIN_BLOCKS)
+__global__ void __launch_bounds__(kThreads, RGBDSEG_FUSED_MIN_BLOCKS(kElide))
     k_fused_ldg(const __grid_constant__ FusedArgs a) {
     const size_t i = (size_t)blockIdx.x * kThreads + threadIdx.x;
     const bool active = i < a.n;
