@@ -203,6 +203,10 @@ __global__ void __launch_bounds__(kThreads)
 // Resident blocks per SM: the dense variant is HBM-bound at 3 (80 regs);
 // the elided one is latency-bound and gains from 4 (64 regs, 32 warps/SM)
 // despite a few spilled words (profiles/variants_r01.json).
+// Depth mixture prefetched into L1 during the colour step (see fused_pixel).
+#ifndef RGBDSEG_PREFETCH_DEPTH
+#define RGBDSEG_PREFETCH_DEPTH 1
+#endif
 #ifndef RGBDSEG_FUSED_MIN_BLOCKS
 #define RGBDSEG_FUSED_MIN_BLOCKS(elide) ((elide) ? 4 : 3)
 #endif
@@ -226,8 +230,17 @@ __device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i, uint32
     const int cpt0 = a.fuse ? (int)ld_stream(a.cpt + i) : 0;
     Mixture<MC, 3> cm;
     Mixture<MD, 1> dm;
+#if RGBDSEG_PREFETCH_DEPTH
+    // The depth mixture goes to L1 now (no registers held) and into registers
+    // only after the colour step, lowering the colour step's register peak.
+#pragma unroll
+    for (int p = 0; p < bank_planes(MD, 1); ++p)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(ds + p * kBlockPx));
+    load_mix(cs, cm);
+#else
     load_mix(cs, cm);
     load_mix(ds, dm);
+#endif
 
     // ---- colour stream (segment_color) ----
     float cw_old[MC];
@@ -243,6 +256,9 @@ __device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i, uint32
 
     // ---- depth stream (segment_depth): raw 0 = no return ----
     uint32_t ld = 0;
+#if RGBDSEG_PREFETCH_DEPTH
+    if (raw != 0) load_mix(ds, dm);
+#endif
     if (raw != 0) {
         const float vd[1] = {(float)raw};
         float dw_old[MD];
