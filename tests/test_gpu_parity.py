@@ -661,3 +661,29 @@ def test_acceptance_quality_criteria_on_gpu(R, cuda, scenario):
         assert abs(mean["fused"] - 0.9870) < 2e-3 and abs(mean["depth"] - 0.9984) < 2e-3
     else:
         assert mean["fused"] >= 0.80
+
+
+@pytest.mark.parametrize("mc,md", [(3, 5), (5, 3), (4, 4), (3, 3), (5, 4)])
+@pytest.mark.parametrize("variant", ["ldg", "auto"])
+def test_processor_mixed_component_counts(R, port, mc, md, variant):
+    """Every (colour M, depth M) instantiation of K1 against the oracle,
+    with non-default rates and a counter limit of 2."""
+    w, h = 72, 40
+    cfg = R.RunConfig.defaults()
+    cfg.color_gmm.components, cfg.depth_gmm.components = mc, md
+    cfg.color_gmm.learning_rate, cfg.depth_gmm.background_threshold = 0.1, 0.7
+    cfg.fusion_counter_limit, cfg.fusion_initial_label = 2, 1
+    proc = R.SequenceProcessor(w, h, cfg, variant=variant)
+    oc = O.color_cfg(mc, learning_rate=0.1)
+    od = O.depth_cfg(md, background_threshold=0.7)
+    orc = O.PortProcessor(port, w * h, oc, od, limit=2, initial_label=1)
+    sc = O.PortScene(port, "B", w, h, seed=9)
+    for f in range(60):
+        fr = sc.render(25 + f)
+        d = holes(fr.depth, f)
+        fm = proc.process(fr.r, fr.g, fr.b, d)
+        for x, y in zip((fm.rgb, fm.depth, fm.fused), orc.process(fr.r, fr.g, fr.b, d)):
+            assert np.array_equal(x.ravel(), y), (mc, md, f)
+    assert proc.color_bank().planes().tobytes() == orc.color.planes().tobytes()
+    assert proc.depth_bank().planes().tobytes() == orc.depth.planes().tobytes()
+    assert np.array_equal(proc.fusion_state().cpt.ravel(), orc.cpt)
