@@ -81,14 +81,28 @@ MixCfg to_k(const rgbdseg_mixture_cfg& c) {
                   c.initial_sigma, c.initial_weight, c.variance_floor, fast};
 }
 
+// Pointer classification with a small direct-mapped cache: a host address
+// can never become a device address under UVA (disjoint ranges), so a cached
+// "device" / "host" verdict stays valid for the address; callers pass the
+// same frame buffers every frame.
 bool on_device(const void* p) {
     if (!p) return false;
+    struct Entry {
+        const void* p;
+        bool dev;
+    };
+    thread_local Entry cache[64] = {};
+    const size_t slot = (reinterpret_cast<uintptr_t>(p) >> 8) & 63;
+    if (cache[slot].p == p) return cache[slot].dev;
     cudaPointerAttributes a;
+    bool dev = false;
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
         cudaGetLastError();
-        return false;
+    } else {
+        dev = a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
     }
-    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+    cache[slot] = Entry{p, dev};
+    return dev;
 }
 
 size_t pitch_for(size_t npx) { return (npx + 63) & ~size_t(63); }  // 256-byte planes
@@ -645,10 +659,7 @@ void rgbdseg_processor_destroy(rgbdseg_processor* p) {
     for (cudaStream_t s : {p->sc, p->sh2d, p->sd2h})
         if (s) cudaStreamSynchronize(s);
     for (auto& sl : p->slot) {
-        dfree(sl.r);
-        dfree(sl.g);
-        dfree(sl.b);
-        dfree(sl.d);
+        dfree(sl.r);  // g, b, d live in the same allocation
         dfree(sl.rgbm);
         dfree(sl.depm);
         dfree(sl.gt);
@@ -726,10 +737,13 @@ int rgbdseg_processor_create(const rgbdseg_processor_cfg* cfg, rgbdseg_processor
 static int ensure_slots(rgbdseg_processor* p) {
     for (auto& sl : p->slot) {
         if (sl.r) continue;
-        int rc = dalloc(&sl.r, p->chunk);
-        if (!rc) rc = dalloc(&sl.g, p->chunk);
-        if (!rc) rc = dalloc(&sl.b, p->chunk);
-        if (!rc) rc = dalloc(&sl.d, p->chunk);
+        // r | g | b | depth back to back, so a planar host frame whose planes
+        // are contiguous moves in one DMA per chunk
+        int rc = dalloc(&sl.r, 5 * p->chunk);
+        if (rc) return rc;
+        sl.g = sl.r + p->chunk;
+        sl.b = sl.g + p->chunk;
+        sl.d = reinterpret_cast<uint16_t*>(sl.b + p->chunk);
         if (!rc) rc = dalloc(&sl.rgbm, p->chunk);
         if (!rc) rc = dalloc(&sl.depm, p->chunk);
         if (!rc) rc = dalloc(&sl.gt, p->chunk);
@@ -871,6 +885,10 @@ static int submit_impl(rgbdseg_processor* p, const uint8_t* r, const uint8_t* g,
         return RGBDSEG_OK;
     }
     if (int rc = ensure_slots(p)) return rc;
+    // planar host frame: the four planes back to back in one host buffer
+    const bool planar = !dr && !dg && !db && !dd && g == r + p->npx && b == g + p->npx &&
+                        reinterpret_cast<const uint8_t*>(depth) == b + p->npx &&
+                        p->nchunks == 1;
     for (int c = 0; c < p->nchunks; ++c) {
         const size_t lo = (size_t)c * p->chunk;
         if (lo >= p->npx) break;
@@ -882,10 +900,17 @@ static int submit_impl(rgbdseg_processor* p, const uint8_t* r, const uint8_t* g,
         a.g = dg ? g + lo : sl.g;
         a.b = db ? b + lo : sl.b;
         a.d = dd ? depth + lo : sl.d;
-        if (!dr) CU(cudaMemcpyAsync(sl.r, r + lo, n, cudaMemcpyDefault, p->sh2d));
-        if (!dg) CU(cudaMemcpyAsync(sl.g, g + lo, n, cudaMemcpyDefault, p->sh2d));
-        if (!db) CU(cudaMemcpyAsync(sl.b, b + lo, n, cudaMemcpyDefault, p->sh2d));
-        if (!dd) CU(cudaMemcpyAsync(sl.d, depth + lo, n * 2, cudaMemcpyDefault, p->sh2d));
+        if (planar && n == p->chunk) {  // r|g|b|depth contiguous on the host: one DMA
+            CU(cudaMemcpyAsync(sl.r, r + lo, 5 * n, cudaMemcpyDefault, p->sh2d));
+        } else if (planar && n == p->npx && lo == 0) {
+            CU(cudaMemcpy2DAsync(sl.r, p->chunk, r, n, n, 3, cudaMemcpyDefault, p->sh2d));
+            CU(cudaMemcpyAsync(sl.d, depth, 2 * n, cudaMemcpyDefault, p->sh2d));
+        } else {
+            if (!dr) CU(cudaMemcpyAsync(sl.r, r + lo, n, cudaMemcpyDefault, p->sh2d));
+            if (!dg) CU(cudaMemcpyAsync(sl.g, g + lo, n, cudaMemcpyDefault, p->sh2d));
+            if (!db) CU(cudaMemcpyAsync(sl.b, b + lo, n, cudaMemcpyDefault, p->sh2d));
+            if (!dd) CU(cudaMemcpyAsync(sl.d, depth + lo, n * 2, cudaMemcpyDefault, p->sh2d));
+        }
         a.gt = gt ? (dgt ? gt + lo : sl.gt) : nullptr;
         if (gt && !dgt) CU(cudaMemcpyAsync(sl.gt, gt + lo, n, cudaMemcpyDefault, p->sh2d));
         CU(cudaEventRecord(sl.h2d_done, p->sh2d));

@@ -297,11 +297,19 @@ def test_host_chunked_pipeline_equals_device_path(R, cuda):
     for f in range(40):
         fr = R.render_scenario("B", w, h, 30 + f, streams=S, seed0=9)
         host = {k: to_np(v) for k, v in fr.items()}
-        if f % 2:  # exercise submit/sync with pinned host buffers too
+        if f % 3 == 1:  # exercise submit/sync with pinned host buffers too
             pinned = {k: pinned_copy(v) for k, v in host.items()}
             fa, fa_t = pinned_copy(np.zeros((S, h, w), np.uint8))
             a.submit(*(pinned[k][0] for k in ("r", "g", "b", "depth")), fused=fa)
             a.sync()
+        elif f % 3 == 2:  # one planar host buffer r|g|b|depth (single-DMA path)
+            n = S * h * w
+            buf = np.empty(5 * n, np.uint8)
+            for i, k in enumerate("rgb"):
+                buf[i * n:(i + 1) * n] = host[k].ravel()
+            buf[3 * n:].view(np.uint16)[:] = host["depth"].ravel()
+            planes = [buf[i * n:(i + 1) * n].reshape(S, h, w) for i in range(3)]
+            fa = a.process(*planes, buf[3 * n:].view(np.uint16).reshape(S, h, w)).fused
         else:
             fa = a.process(host["r"], host["g"], host["b"], host["depth"]).fused
         fb = torch.empty((S, h, w), dtype=torch.uint8, device=cuda)
@@ -687,3 +695,30 @@ def test_processor_mixed_component_counts(R, port, mc, md, variant):
     assert proc.color_bank().planes().tobytes() == orc.color.planes().tobytes()
     assert proc.depth_bank().planes().tobytes() == orc.depth.planes().tobytes()
     assert np.array_equal(proc.fusion_state().cpt.ravel(), orc.cpt)
+
+
+@pytest.mark.parametrize("w,h,S", [(64, 32, 1), (50, 30, 2)])
+def test_planar_single_chunk_host_frames(R, cuda, w, h, S):
+    """Planar host frames (r|g|b|depth in one buffer) take the single-DMA
+    path when the frame is one chunk -- both when the plane size equals the
+    slot pitch (64x32) and when it does not (50x30, a 2-D copy) -- and give
+    the device path's bits."""
+    import torch
+
+    cfg = R.RunConfig.defaults()
+    a = R.SequenceProcessor(w, h, cfg, streams=S)
+    b = R.SequenceProcessor(w, h, cfg, streams=S)
+    n = S * w * h
+    for f in range(20):
+        fr = R.render_scenario("A", w, h, 95 + f, streams=S, seed0=4)
+        host = {k: to_np(v) for k, v in fr.items()}
+        buf, keep = pinned_copy(np.zeros(5 * n, np.uint8))
+        for i, k in enumerate("rgb"):
+            buf[i * n:(i + 1) * n] = host[k].ravel()
+        buf[3 * n:].view(np.uint16)[:] = host["depth"].ravel()
+        planes = [buf[i * n:(i + 1) * n].reshape(S, h, w) for i in range(3)]
+        fa = a.process(*planes, buf[3 * n:].view(np.uint16).reshape(S, h, w), want=("fused",)).fused
+        fb = torch.empty((S, h, w), dtype=torch.uint8, device=cuda)
+        b.process(fr["r"], fr["g"], fr["b"], fr["depth"], want=(), out={"fused": fb})
+        assert np.array_equal(np.asarray(fa).reshape(S, h, w), fb.cpu().numpy()), f
+    assert a.color_bank().state_equals(b.color_bank())
