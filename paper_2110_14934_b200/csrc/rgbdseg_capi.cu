@@ -188,11 +188,13 @@ struct rgbdseg_fusion {
     Scratch s_rgb, s_dep;
 };
 
+// A device staging slot for one chunk of host frames: r | g | b | depth back
+// to back (a planar host frame moves in one or two DMAs), mask outputs and
+// the ground truth for the evaluation epilogue.
 struct Slot {
     uint8_t *r = nullptr, *g = nullptr, *b = nullptr, *gt = nullptr;
     uint16_t* d = nullptr;
-    uint8_t *rgbm = nullptr, *depm = nullptr;
-    cudaEvent_t h2d_done = nullptr, k_done = nullptr, d2h_done = nullptr;
+    uint8_t *rgbm = nullptr, *depm = nullptr, *fused = nullptr;
 };
 
 struct rgbdseg_processor {
@@ -200,17 +202,20 @@ struct rgbdseg_processor {
     rgbdseg_bank* color = nullptr;
     rgbdseg_bank* depth = nullptr;
     rgbdseg_fusion* fusion = nullptr;
-    cudaStream_t sc = nullptr, sh2d = nullptr, sd2h = nullptr;
+    // Host frames: chunk c of every frame runs H2D -> K1 -> D2H on cs[c % 2]
+    // with slot[c % 2].  Stream order alone provides every dependency (the
+    // same pixels of consecutive frames stay on one stream; a slot is reused
+    // only by its own stream), and the two streams overlap each other.
+    cudaStream_t cs[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2] = {nullptr, nullptr};  // cross-stream joins (mode switches, counts)
     size_t npx = 0, chunk = 0;
     int nchunks = 1;
     Slot slot[2];
-    std::vector<cudaEvent_t> chunk_d2h;  // per chunk: last D2H reading fusion.out of it
-    uint64_t seq = 0;
+    int last_mode = 0;  // 0 none, 1 host chunks (both streams), 2 single stream cs[0]
     int64_t frames = 0;
     int variant = kAuto;
     // unregistered sequences: whole-frame scratch (inputs, masks, splat)
     Scratch u_in, u_masks, u_gt;
-    cudaEvent_t u_h2d = nullptr, u_k = nullptr;
     Scratch counts;  // evaluation epilogue: [streams][3][4] uint64
 };
 
@@ -656,22 +661,19 @@ void rgbdseg_processor_defaults(rgbdseg_processor_cfg* c, int width, int height)
 void rgbdseg_processor_destroy(rgbdseg_processor* p) {
     if (!p) return;
     DeviceGuard g(p->cfg.device);
-    for (cudaStream_t s : {p->sc, p->sh2d, p->sd2h})
-        if (s) cudaStreamSynchronize(s);
+    for (cudaStream_t st : p->cs)
+        if (st) cudaStreamSynchronize(st);
     for (auto& sl : p->slot) {
         dfree(sl.r);  // g, b, d live in the same allocation
         dfree(sl.rgbm);
         dfree(sl.depm);
+        dfree(sl.fused);
         dfree(sl.gt);
-        for (cudaEvent_t ev : {sl.h2d_done, sl.k_done, sl.d2h_done})
-            if (ev) cudaEventDestroy(ev);
     }
-    for (cudaEvent_t ev : p->chunk_d2h)
-        if (ev) cudaEventDestroy(ev);
-    for (cudaEvent_t ev : {p->u_h2d, p->u_k})
-        if (ev) cudaEventDestroy(ev);
-    for (cudaStream_t s : {p->sc, p->sh2d, p->sd2h})
-        if (s) cudaStreamDestroy(s);
+    for (cudaEvent_t e : p->ev)
+        if (e) cudaEventDestroy(e);
+    for (cudaStream_t st : p->cs)
+        if (st) cudaStreamDestroy(st);
     rgbdseg_bank_destroy(p->color);
     rgbdseg_bank_destroy(p->depth);
     rgbdseg_fusion_destroy(p->fusion);
@@ -707,23 +709,18 @@ int rgbdseg_processor_create(const rgbdseg_processor_cfg* cfg, rgbdseg_processor
                                    cfg->fusion_initial_label, cfg->fusion_counter_limit,
                                    cfg->device, &p->fusion);
     if (!rc) {
-        // Host frames stream through two device slots in chunks so the H2D of
-        // chunk k+1, the kernel of chunk k and the D2H of chunk k-1 overlap.
+        // >= 2 chunks so the two streams overlap even for one small frame;
+        // chunk boundaries on 64-pixel (two tiled-block) multiples.
         int chunks = cfg->host_chunks;
-        if (chunks <= 0) chunks = (int)std::min<size_t>(8, std::max<size_t>(1, p->npx >> 21));
+        if (chunks <= 0) chunks = (int)std::min<size_t>(8, std::max<size_t>(2, p->npx >> 21));
+        if (p->npx < 256) chunks = 1;
         p->nchunks = chunks;
         p->chunk = pitch_for((p->npx + chunks - 1) / chunks);
         cudaError_t e = cudaSuccess;
-        for (cudaStream_t* s : {&p->sc, &p->sh2d, &p->sd2h})
-            if (e == cudaSuccess) e = cudaStreamCreateWithFlags(s, cudaStreamNonBlocking);
-        for (auto& sl : p->slot)
-            for (cudaEvent_t* ev : {&sl.h2d_done, &sl.k_done, &sl.d2h_done})
-                if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
-        p->chunk_d2h.assign(chunks, nullptr);
-        for (auto& ev : p->chunk_d2h)
+        for (cudaStream_t& st : p->cs)
+            if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+        for (cudaEvent_t& ev : p->ev)
             if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-        for (cudaEvent_t* ev : {&p->u_h2d, &p->u_k})
-            if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
         if (e != cudaSuccess) rc = cuda_fail(e, "processor_create");
     }
     if (rc) {
@@ -737,8 +734,6 @@ int rgbdseg_processor_create(const rgbdseg_processor_cfg* cfg, rgbdseg_processor
 static int ensure_slots(rgbdseg_processor* p) {
     for (auto& sl : p->slot) {
         if (sl.r) continue;
-        // r | g | b | depth back to back, so a planar host frame whose planes
-        // are contiguous moves in one DMA per chunk
         int rc = dalloc(&sl.r, 5 * p->chunk);
         if (rc) return rc;
         sl.g = sl.r + p->chunk;
@@ -746,9 +741,25 @@ static int ensure_slots(rgbdseg_processor* p) {
         sl.d = reinterpret_cast<uint16_t*>(sl.b + p->chunk);
         if (!rc) rc = dalloc(&sl.rgbm, p->chunk);
         if (!rc) rc = dalloc(&sl.depm, p->chunk);
+        if (!rc) rc = dalloc(&sl.fused, p->chunk);
         if (!rc) rc = dalloc(&sl.gt, p->chunk);
         if (rc) return rc;
     }
+    return RGBDSEG_OK;
+}
+
+// Order work about to be queued in `mode` after everything queued before
+// in the other mode (host chunks use both streams; the device path and the
+// unregistered path use cs[0]).
+static int switch_mode(rgbdseg_processor* p, int mode) {
+    if (p->last_mode == 1 && mode == 2) {  // join cs[1] into cs[0]
+        CU(cudaEventRecord(p->ev[1], p->cs[1]));
+        CU(cudaStreamWaitEvent(p->cs[0], p->ev[1], 0));
+    } else if (p->last_mode == 2 && mode == 1) {  // fork cs[0] into cs[1]
+        CU(cudaEventRecord(p->ev[0], p->cs[0]));
+        CU(cudaStreamWaitEvent(p->cs[1], p->ev[0], 0));
+    }
+    p->last_mode = mode;
     return RGBDSEG_OK;
 }
 
@@ -772,6 +783,8 @@ static int submit_unregistered(rgbdseg_processor* p, const uint8_t* r, const uin
                                unsigned long long* dcounts) {
     const size_t n = p->npx;
     const int w = p->cfg.width, h = p->cfg.height, S = p->cfg.streams;
+    cudaStream_t st = p->cs[0];
+    if (int rc = switch_mode(p, 2)) return rc;
     void* ibuf;
     if (int rc = p->u_in.get(5 * n, &ibuf)) return rc;
     void* mbuf;
@@ -779,8 +792,6 @@ static int submit_unregistered(rgbdseg_processor* p, const uint8_t* r, const uin
     uint8_t* in = static_cast<uint8_t*>(ibuf);
     uint8_t *rgbm = static_cast<uint8_t*>(mbuf), *depm = rgbm + n, *splat = depm + n,
             *tmp = splat + n, *reg = tmp + n;
-    // the previous frame's D2H must have drained the mask scratch
-    CU(cudaStreamWaitEvent(p->sh2d, p->u_k, 0));
     const uint8_t* src[4] = {r, g, b, reinterpret_cast<const uint8_t*>(depth)};
     const uint8_t* dev[4];
     size_t off = 0;
@@ -789,14 +800,11 @@ static int submit_unregistered(rgbdseg_processor* p, const uint8_t* r, const uin
         if (on_device(src[k])) {
             dev[k] = src[k];
         } else {
-            CU(cudaMemcpyAsync(in + off, src[k], bytes, cudaMemcpyDefault, p->sh2d));
+            CU(cudaMemcpyAsync(in + off, src[k], bytes, cudaMemcpyDefault, st));
             dev[k] = in + off;
         }
         off += bytes;
     }
-    CU(cudaEventRecord(p->u_h2d, p->sh2d));
-    CU(cudaStreamWaitEvent(p->sc, p->u_h2d, 0));
-    for (cudaEvent_t ev : p->chunk_d2h) CU(cudaStreamWaitEvent(p->sc, ev, 0));
     FusedArgs a = base_args(p);
     a.fuse = 0;
     a.r = dev[0];
@@ -809,26 +817,22 @@ static int submit_unregistered(rgbdseg_processor* p, const uint8_t* r, const uin
     a.cpt = p->fusion->cpt;
     a.base = 0;
     a.n = n;
-    CU(launch_fused(a, p->variant, p->sc));
-    CU(cudaMemsetAsync(splat, 0, n, p->sc));
-    CU(launch_register_splat(depm, a.d, w, h, S, to_dev(p->cfg.rig), w, h, splat, p->sc));
-    CU(launch_dilate(splat, tmp, reg, w, h, S, p->cfg.dilation_radius, p->sc));
+    CU(launch_fused(a, p->variant, st));
+    CU(cudaMemsetAsync(splat, 0, n, st));
+    CU(launch_register_splat(depm, a.d, w, h, S, to_dev(p->cfg.rig), w, h, splat, st));
+    CU(launch_dilate(splat, tmp, reg, w, h, S, p->cfg.dilation_radius, st));
     uint8_t* fcopy = (fused_out && on_device(fused_out)) ? fused_out : nullptr;
     CU(launch_fuse(p->fusion->out, p->fusion->cpt, rgbm, reg, fcopy, p->cfg.fusion_counter_limit,
-                   n, p->sc));
+                   n, st));
     if (gt) {  // evaluation: the three masks against the ground truth
         const void* dgt;
-        if (int rc = stage_in(gt, n, p->u_gt, &dgt, p->sc)) return rc;
+        if (int rc = stage_in(gt, n, p->u_gt, &dgt, st)) return rc;
         const uint8_t* preds[3] = {rgbm, depm, p->fusion->out};
-        CU(launch_confusion(preds, 3, (const uint8_t*)dgt, n, (size_t)w * h, dcounts, p->sc));
+        CU(launch_confusion(preds, 3, (const uint8_t*)dgt, n, (size_t)w * h, dcounts, st));
     }
-    CU(cudaEventRecord(p->u_k, p->sc));
-    CU(cudaStreamWaitEvent(p->sd2h, p->u_k, 0));
-    if (fused_out && !fcopy) CU(cudaMemcpyAsync(fused_out, p->fusion->out, n, cudaMemcpyDefault, p->sd2h));
-    if (rgb_out) CU(cudaMemcpyAsync(rgb_out, rgbm, n, cudaMemcpyDefault, p->sd2h));
-    if (depth_out) CU(cudaMemcpyAsync(depth_out, depm, n, cudaMemcpyDefault, p->sd2h));
-    CU(cudaEventRecord(p->u_k, p->sd2h));
-    if (!p->chunk_d2h.empty()) CU(cudaEventRecord(p->chunk_d2h[0], p->sd2h));
+    if (fused_out && !fcopy) CU(cudaMemcpyAsync(fused_out, p->fusion->out, n, cudaMemcpyDefault, st));
+    if (rgb_out) CU(cudaMemcpyAsync(rgb_out, rgbm, n, cudaMemcpyDefault, st));
+    if (depth_out) CU(cudaMemcpyAsync(depth_out, depm, n, cudaMemcpyDefault, st));
     ++p->frames;
     return RGBDSEG_OK;
 }
@@ -838,31 +842,35 @@ static int submit_impl(rgbdseg_processor* p, const uint8_t* r, const uint8_t* g,
                        uint8_t* depth_out, const uint8_t* gt, int64_t* counts_out) {
     if (!r || !g || !b || !depth) return fail(RGBDSEG_EINVAL, "process: null input plane");
     if (gt && !counts_out) return fail(RGBDSEG_EINVAL, "process: ground truth without counts");
+    const bool dr = on_device(r), dg = on_device(g), db = on_device(b), dd = on_device(depth);
+    const bool dfo = on_device(fused_out), dro = on_device(rgb_out), ddo = on_device(depth_out);
+    const bool dgt = gt && on_device(gt);
+    const bool all_device = dr && dg && db && dd && (!fused_out || dfo) && (!rgb_out || dro) &&
+                            (!depth_out || ddo) && (!gt || dgt);
+    const bool single = !p->cfg.registered || all_device;
+    if (int rc = switch_mode(p, single ? 2 : 1)) return rc;
     unsigned long long* dcounts = nullptr;
     const size_t ncnt = (size_t)p->cfg.streams * 12;
     if (gt) {
         void* c;
         if (int rc = p->counts.get(ncnt * sizeof(unsigned long long), &c)) return rc;
         dcounts = static_cast<unsigned long long*>(c);
-        CU(cudaMemsetAsync(dcounts, 0, ncnt * sizeof(unsigned long long), p->sc));
+        CU(cudaMemsetAsync(dcounts, 0, ncnt * sizeof(unsigned long long), p->cs[0]));
+        if (!single) {  // both chunk streams accumulate into the zeroed counters
+            CU(cudaEventRecord(p->ev[0], p->cs[0]));
+            CU(cudaStreamWaitEvent(p->cs[1], p->ev[0], 0));
+        }
     }
-    const bool dgt = gt && on_device(gt);
     if (!p->cfg.registered) {
         int rc = submit_unregistered(p, r, g, b, depth, fused_out, rgb_out, depth_out, gt, dcounts);
         if (!rc && gt)
-            CU(cudaMemcpyAsync(counts_out, dcounts, ncnt * 8, cudaMemcpyDefault, p->sd2h));
+            CU(cudaMemcpyAsync(counts_out, dcounts, ncnt * 8, cudaMemcpyDefault, p->cs[0]));
         return rc;
     }
-    const bool dr = on_device(r), dg = on_device(g), db = on_device(b), dd = on_device(depth);
-    const bool dfo = on_device(fused_out), dro = on_device(rgb_out), ddo = on_device(depth_out);
-    const bool all_device = dr && dg && db && dd && (!fused_out || dfo) && (!rgb_out || dro) &&
-                            (!depth_out || ddo);
     FusedArgs a = base_args(p);
-    a.out = p->fusion->out;
-    a.cpt = p->fusion->cpt;
     a.counts = dcounts;
     a.stream_px = (size_t)p->cfg.width * p->cfg.height;
-    if (all_device && (!gt || dgt)) {  // device-resident frames: one launch over every pixel
+    if (all_device) {  // device-resident frames: one launch over every pixel
         a.r = r;
         a.g = g;
         a.b = b;
@@ -870,76 +878,61 @@ static int submit_impl(rgbdseg_processor* p, const uint8_t* r, const uint8_t* g,
         a.rgb_mask = rgb_out;
         a.depth_mask = depth_out;
         a.fused_copy = fused_out;
+        a.out = p->fusion->out;
+        a.cpt = p->fusion->cpt;
         a.base = 0;
         a.n = p->npx;
         a.gt = gt;
-        for (cudaEvent_t ev : p->chunk_d2h)  // a host-frame emit may still read out
-            CU(cudaStreamWaitEvent(p->sc, ev, 0));
-        CU(launch_fused(a, p->variant, p->sc));
-        if (gt) {
-            CU(cudaEventRecord(p->u_k, p->sc));
-            CU(cudaStreamWaitEvent(p->sd2h, p->u_k, 0));
-            CU(cudaMemcpyAsync(counts_out, dcounts, ncnt * 8, cudaMemcpyDefault, p->sd2h));
-        }
+        CU(launch_fused(a, p->variant, p->cs[0]));
+        if (gt) CU(cudaMemcpyAsync(counts_out, dcounts, ncnt * 8, cudaMemcpyDefault, p->cs[0]));
         ++p->frames;
         return RGBDSEG_OK;
     }
     if (int rc = ensure_slots(p)) return rc;
     // planar host frame: the four planes back to back in one host buffer
     const bool planar = !dr && !dg && !db && !dd && g == r + p->npx && b == g + p->npx &&
-                        reinterpret_cast<const uint8_t*>(depth) == b + p->npx &&
-                        p->nchunks == 1;
+                        reinterpret_cast<const uint8_t*>(depth) == b + p->npx;
     for (int c = 0; c < p->nchunks; ++c) {
         const size_t lo = (size_t)c * p->chunk;
         if (lo >= p->npx) break;
         const size_t n = std::min(p->chunk, p->npx - lo);
-        Slot& sl = p->slot[p->seq++ & 1];
-        // ingest: wait until the previous kernel on this slot consumed it
-        CU(cudaStreamWaitEvent(p->sh2d, sl.k_done, 0));
+        Slot& sl = p->slot[c & 1];
+        cudaStream_t st = p->cs[c & 1];
+        // ingest
+        if (planar) {  // r, g, b rows of this chunk in one 2-D copy, depth in one
+            CU(cudaMemcpy2DAsync(sl.r, p->chunk, r + lo, p->npx, n, 3, cudaMemcpyDefault, st));
+            CU(cudaMemcpyAsync(sl.d, depth + lo, 2 * n, cudaMemcpyDefault, st));
+        } else {
+            if (!dr) CU(cudaMemcpyAsync(sl.r, r + lo, n, cudaMemcpyDefault, st));
+            if (!dg) CU(cudaMemcpyAsync(sl.g, g + lo, n, cudaMemcpyDefault, st));
+            if (!db) CU(cudaMemcpyAsync(sl.b, b + lo, n, cudaMemcpyDefault, st));
+            if (!dd) CU(cudaMemcpyAsync(sl.d, depth + lo, n * 2, cudaMemcpyDefault, st));
+        }
+        if (gt && !dgt) CU(cudaMemcpyAsync(sl.gt, gt + lo, n, cudaMemcpyDefault, st));
+        // process
         a.r = dr ? r + lo : sl.r;
         a.g = dg ? g + lo : sl.g;
         a.b = db ? b + lo : sl.b;
         a.d = dd ? depth + lo : sl.d;
-        if (planar && n == p->chunk) {  // r|g|b|depth contiguous on the host: one DMA
-            CU(cudaMemcpyAsync(sl.r, r + lo, 5 * n, cudaMemcpyDefault, p->sh2d));
-        } else if (planar && n == p->npx && lo == 0) {
-            CU(cudaMemcpy2DAsync(sl.r, p->chunk, r, n, n, 3, cudaMemcpyDefault, p->sh2d));
-            CU(cudaMemcpyAsync(sl.d, depth, 2 * n, cudaMemcpyDefault, p->sh2d));
-        } else {
-            if (!dr) CU(cudaMemcpyAsync(sl.r, r + lo, n, cudaMemcpyDefault, p->sh2d));
-            if (!dg) CU(cudaMemcpyAsync(sl.g, g + lo, n, cudaMemcpyDefault, p->sh2d));
-            if (!db) CU(cudaMemcpyAsync(sl.b, b + lo, n, cudaMemcpyDefault, p->sh2d));
-            if (!dd) CU(cudaMemcpyAsync(sl.d, depth + lo, n * 2, cudaMemcpyDefault, p->sh2d));
-        }
         a.gt = gt ? (dgt ? gt + lo : sl.gt) : nullptr;
-        if (gt && !dgt) CU(cudaMemcpyAsync(sl.gt, gt + lo, n, cudaMemcpyDefault, p->sh2d));
-        CU(cudaEventRecord(sl.h2d_done, p->sh2d));
-        // process: inputs landed, previous emit of this slot's masks and of
-        // this chunk's fused labels finished
-        CU(cudaStreamWaitEvent(p->sc, sl.h2d_done, 0));
-        CU(cudaStreamWaitEvent(p->sc, sl.d2h_done, 0));
-        CU(cudaStreamWaitEvent(p->sc, p->chunk_d2h[c], 0));
         a.rgb_mask = rgb_out ? (dro ? rgb_out + lo : sl.rgbm) : nullptr;
         a.depth_mask = depth_out ? (ddo ? depth_out + lo : sl.depm) : nullptr;
-        a.fused_copy = (fused_out && dfo) ? fused_out + lo : nullptr;
+        a.fused_copy = fused_out ? (dfo ? fused_out + lo : sl.fused) : nullptr;
         a.base = lo;
         a.n = n;
         a.out = p->fusion->out + lo;
         a.cpt = p->fusion->cpt + lo;
-        CU(launch_fused(a, p->variant, p->sc));
-        CU(cudaEventRecord(sl.k_done, p->sc));
+        CU(launch_fused(a, p->variant, st));
         // emit
-        CU(cudaStreamWaitEvent(p->sd2h, sl.k_done, 0));
-        if (fused_out && !dfo)
-            CU(cudaMemcpyAsync(fused_out + lo, p->fusion->out + lo, n, cudaMemcpyDefault, p->sd2h));
-        if (rgb_out && !dro)
-            CU(cudaMemcpyAsync(rgb_out + lo, sl.rgbm, n, cudaMemcpyDefault, p->sd2h));
-        if (depth_out && !ddo)
-            CU(cudaMemcpyAsync(depth_out + lo, sl.depm, n, cudaMemcpyDefault, p->sd2h));
-        CU(cudaEventRecord(sl.d2h_done, p->sd2h));
-        CU(cudaEventRecord(p->chunk_d2h[c], p->sd2h));
+        if (fused_out && !dfo) CU(cudaMemcpyAsync(fused_out + lo, sl.fused, n, cudaMemcpyDefault, st));
+        if (rgb_out && !dro) CU(cudaMemcpyAsync(rgb_out + lo, sl.rgbm, n, cudaMemcpyDefault, st));
+        if (depth_out && !ddo) CU(cudaMemcpyAsync(depth_out + lo, sl.depm, n, cudaMemcpyDefault, st));
     }
-    if (gt) CU(cudaMemcpyAsync(counts_out, dcounts, ncnt * 8, cudaMemcpyDefault, p->sd2h));
+    if (gt) {  // join both streams' counters, then copy them out
+        CU(cudaEventRecord(p->ev[1], p->cs[1]));
+        CU(cudaStreamWaitEvent(p->cs[0], p->ev[1], 0));
+        CU(cudaMemcpyAsync(counts_out, dcounts, ncnt * 8, cudaMemcpyDefault, p->cs[0]));
+    }
     ++p->frames;
     return RGBDSEG_OK;
 }
@@ -991,9 +984,8 @@ int rgbdseg_confusion_counts(const uint8_t* pred, const uint8_t* gt, size_t npx,
 
 int rgbdseg_processor_sync(rgbdseg_processor* p) {
     GUARD(p->cfg.device);
-    CU(cudaStreamSynchronize(p->sh2d));
-    CU(cudaStreamSynchronize(p->sc));
-    CU(cudaStreamSynchronize(p->sd2h));
+    CU(cudaStreamSynchronize(p->cs[0]));
+    CU(cudaStreamSynchronize(p->cs[1]));
     return RGBDSEG_OK;
 }
 
@@ -1009,7 +1001,7 @@ int64_t rgbdseg_processor_frames(const rgbdseg_processor* p) { return p->frames;
 rgbdseg_bank* rgbdseg_processor_color_bank(rgbdseg_processor* p) { return p->color; }
 rgbdseg_bank* rgbdseg_processor_depth_bank(rgbdseg_processor* p) { return p->depth; }
 rgbdseg_fusion* rgbdseg_processor_fusion(rgbdseg_processor* p) { return p->fusion; }
-void* rgbdseg_processor_stream(rgbdseg_processor* p) { return (void*)p->sc; }
+void* rgbdseg_processor_stream(rgbdseg_processor* p) { return (void*)p->cs[0]; }
 
 int rgbdseg_processor_set_variant(rgbdseg_processor* p, int variant) {
     if (variant < kAuto || variant > kLdgElide) return fail(RGBDSEG_EINVAL, "unknown kernel variant");
