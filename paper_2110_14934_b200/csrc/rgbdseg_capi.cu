@@ -208,6 +208,7 @@ struct rgbdseg_processor {
     // only by its own stream), and the two streams overlap each other.
     cudaStream_t cs[2] = {nullptr, nullptr};
     cudaEvent_t ev[2] = {nullptr, nullptr};  // cross-stream joins (mode switches, counts)
+    cudaEvent_t ev_k[2] = {nullptr, nullptr};  // single-chunk frames: K1 of the frame on cs[i]
     size_t npx = 0, chunk = 0;
     int nchunks = 1;
     Slot slot[2];
@@ -672,6 +673,8 @@ void rgbdseg_processor_destroy(rgbdseg_processor* p) {
     }
     for (cudaEvent_t e : p->ev)
         if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : p->ev_k)
+        if (e) cudaEventDestroy(e);
     for (cudaStream_t st : p->cs)
         if (st) cudaStreamDestroy(st);
     rgbdseg_bank_destroy(p->color);
@@ -709,17 +712,20 @@ int rgbdseg_processor_create(const rgbdseg_processor_cfg* cfg, rgbdseg_processor
                                    cfg->fusion_initial_label, cfg->fusion_counter_limit,
                                    cfg->device, &p->fusion);
     if (!rc) {
-        // >= 2 chunks so the two streams overlap even for one small frame;
-        // chunk boundaries on 64-pixel (two tiled-block) multiples.
+        // Large frames: up to 8 chunks of >= 2 Mpx, chunk c on stream c % 2.
+        // Smaller frames stay one chunk (per-call CPU cost dominates) and
+        // alternate streams frame by frame.  Chunk boundaries fall on
+        // 64-pixel (two tiled-block) multiples.
         int chunks = cfg->host_chunks;
-        if (chunks <= 0) chunks = (int)std::min<size_t>(8, std::max<size_t>(2, p->npx >> 21));
-        if (p->npx < 256) chunks = 1;
+        if (chunks <= 0) chunks = (int)std::min<size_t>(8, std::max<size_t>(1, p->npx >> 21));
         p->nchunks = chunks;
         p->chunk = pitch_for((p->npx + chunks - 1) / chunks);
         cudaError_t e = cudaSuccess;
         for (cudaStream_t& st : p->cs)
             if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
         for (cudaEvent_t& ev : p->ev)
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+        for (cudaEvent_t& ev : p->ev_k)
             if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
         if (e != cudaSuccess) rc = cuda_fail(e, "processor_create");
     }
@@ -892,24 +898,32 @@ static int submit_impl(rgbdseg_processor* p, const uint8_t* r, const uint8_t* g,
     // planar host frame: the four planes back to back in one host buffer
     const bool planar = !dr && !dg && !db && !dd && g == r + p->npx && b == g + p->npx &&
                         reinterpret_cast<const uint8_t*>(depth) == b + p->npx;
+    const bool alternate = p->nchunks == 1;
+    const cudaMemcpyKind h2d = cudaMemcpyHostToDevice, d2h = cudaMemcpyDeviceToHost;
     for (int c = 0; c < p->nchunks; ++c) {
         const size_t lo = (size_t)c * p->chunk;
         if (lo >= p->npx) break;
         const size_t n = std::min(p->chunk, p->npx - lo);
-        Slot& sl = p->slot[c & 1];
-        cudaStream_t st = p->cs[c & 1];
+        const int lane = alternate ? (int)(p->frames & 1) : (c & 1);
+        Slot& sl = p->slot[lane];
+        cudaStream_t st = p->cs[lane];
         // ingest
         if (planar) {  // r, g, b rows of this chunk in one 2-D copy, depth in one
-            CU(cudaMemcpy2DAsync(sl.r, p->chunk, r + lo, p->npx, n, 3, cudaMemcpyDefault, st));
-            CU(cudaMemcpyAsync(sl.d, depth + lo, 2 * n, cudaMemcpyDefault, st));
+            if (n == p->chunk && n == p->npx) {
+                CU(cudaMemcpyAsync(sl.r, r, 5 * n, h2d, st));
+            } else {
+                CU(cudaMemcpy2DAsync(sl.r, p->chunk, r + lo, p->npx, n, 3, h2d, st));
+                CU(cudaMemcpyAsync(sl.d, depth + lo, 2 * n, h2d, st));
+            }
         } else {
-            if (!dr) CU(cudaMemcpyAsync(sl.r, r + lo, n, cudaMemcpyDefault, st));
-            if (!dg) CU(cudaMemcpyAsync(sl.g, g + lo, n, cudaMemcpyDefault, st));
-            if (!db) CU(cudaMemcpyAsync(sl.b, b + lo, n, cudaMemcpyDefault, st));
-            if (!dd) CU(cudaMemcpyAsync(sl.d, depth + lo, n * 2, cudaMemcpyDefault, st));
+            if (!dr) CU(cudaMemcpyAsync(sl.r, r + lo, n, h2d, st));
+            if (!dg) CU(cudaMemcpyAsync(sl.g, g + lo, n, h2d, st));
+            if (!db) CU(cudaMemcpyAsync(sl.b, b + lo, n, h2d, st));
+            if (!dd) CU(cudaMemcpyAsync(sl.d, depth + lo, n * 2, h2d, st));
         }
-        if (gt && !dgt) CU(cudaMemcpyAsync(sl.gt, gt + lo, n, cudaMemcpyDefault, st));
-        // process
+        if (gt && !dgt) CU(cudaMemcpyAsync(sl.gt, gt + lo, n, h2d, st));
+        // process (a single-chunk frame waits for the previous frame's K1,
+        // queued on the other stream)
         a.r = dr ? r + lo : sl.r;
         a.g = dg ? g + lo : sl.g;
         a.b = db ? b + lo : sl.b;
@@ -922,11 +936,13 @@ static int submit_impl(rgbdseg_processor* p, const uint8_t* r, const uint8_t* g,
         a.n = n;
         a.out = p->fusion->out + lo;
         a.cpt = p->fusion->cpt + lo;
+        if (alternate) CU(cudaStreamWaitEvent(st, p->ev_k[lane ^ 1], 0));
         CU(launch_fused(a, p->variant, st));
+        if (alternate) CU(cudaEventRecord(p->ev_k[lane], st));
         // emit
-        if (fused_out && !dfo) CU(cudaMemcpyAsync(fused_out + lo, sl.fused, n, cudaMemcpyDefault, st));
-        if (rgb_out && !dro) CU(cudaMemcpyAsync(rgb_out + lo, sl.rgbm, n, cudaMemcpyDefault, st));
-        if (depth_out && !ddo) CU(cudaMemcpyAsync(depth_out + lo, sl.depm, n, cudaMemcpyDefault, st));
+        if (fused_out && !dfo) CU(cudaMemcpyAsync(fused_out + lo, sl.fused, n, d2h, st));
+        if (rgb_out && !dro) CU(cudaMemcpyAsync(rgb_out + lo, sl.rgbm, n, d2h, st));
+        if (depth_out && !ddo) CU(cudaMemcpyAsync(depth_out + lo, sl.depm, n, d2h, st));
     }
     if (gt) {  // join both streams' counters, then copy them out
         CU(cudaEventRecord(p->ev[1], p->cs[1]));
