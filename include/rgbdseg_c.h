@@ -244,6 +244,34 @@ int rgbdseg_render_scenario(char name, int width, int height, int streams, uint6
                             int frame, uint8_t* r, uint8_t* g, uint8_t* b, uint16_t* depth,
                             uint8_t* gt, int device, void* stream);
 
+/* One frame of an arbitrary ScenarioSpec (synthetic.hpp:61-74), resolved on
+ * the host for that frame index exactly as render_frame does
+ * (synthetic.cpp:124-134): the illumination gain product, each object's
+ * lround'ed waypoint position, and only the shadow / flicker events active
+ * in this frame (in spec order).  At most 4 objects and 16 events of each
+ * kind.  Streams s render with seed seed0 + s. */
+typedef struct rgbdseg_scene_frame {
+    int width, height, streams;
+    uint64_t seed0;
+    int frame;
+    int base_depth_mm, depth_texture_mm, color_texture;
+    double gain;
+    int n_obj;
+    int obj_rect[4][4]; /* x, y, w, h */
+    int obj_color[4][3];
+    int obj_depth_offset_mm[4];
+    int n_shadow;
+    int shadow_rect[16][4];
+    double shadow_darken[16];
+    int n_flicker;
+    int flicker_rect[16][4];
+    double flicker_color_sigma[16], flicker_depth_sigma_mm[16];
+    double noise_color_sigma, noise_depth_sigma_mm;
+} rgbdseg_scene_frame;
+
+int rgbdseg_render_frame(const rgbdseg_scene_frame* frame, uint8_t* r, uint8_t* g, uint8_t* b,
+                         uint16_t* depth, uint8_t* gt, int device, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -33,4 +33,22 @@ from .rgbdseg import (  # noqa: F401
     step_pixel,
 )
 
+from . import dataset, synthetic  # noqa: F401,E402
+from .dataset import (  # noqa: F401,E402
+    MethodSet,
+    SequenceManifest,
+    SequenceSource,
+    SourceError,
+    generate_scenario,
+    generate_scenario_from_spec,
+    generate_synthetic,
+    load_frame,
+    load_manifest,
+    load_mask_png,
+    run_pipeline,
+    save_manifest,
+    segment_sequence,
+)
+from .synthetic import ScenarioSpec, builtin_scenario, parse_scenario_spec  # noqa: F401,E402
+
 __all__ = [n for n in dir() if not n.startswith("_")]

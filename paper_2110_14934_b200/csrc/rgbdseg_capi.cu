@@ -1110,4 +1110,19 @@ int rgbdseg_render_scenario(char name, int width, int height, int streams, uint6
     return RGBDSEG_OK;
 }
 
+int rgbdseg_render_frame(const rgbdseg_scene_frame* f, uint8_t* r, uint8_t* g, uint8_t* b,
+                         uint16_t* depth, uint8_t* gt, int device, void* stream) {
+    static_assert(sizeof(SceneFrame) == sizeof(rgbdseg_scene_frame), "scene frame layout");
+    if (int rc = check_dims(f->width, f->height, f->streams)) return rc;
+    if (f->n_obj < 0 || f->n_obj > 4 || f->n_shadow < 0 || f->n_shadow > 16 || f->n_flicker < 0 ||
+        f->n_flicker > 16)
+        return fail(RGBDSEG_EINVAL, "render_frame: at most 4 objects and 16 events of each kind");
+    GUARD(device);
+    SceneFrame sc;
+    std::memcpy(&sc, f, sizeof sc);
+    CU(launch_render(sc, r, g, b, depth, gt, (cudaStream_t)stream));
+    if (!stream) CU(cudaStreamSynchronize(0));
+    return RGBDSEG_OK;
+}
+
 }  // extern "C"

@@ -110,10 +110,16 @@ class RunConfig:
 
     color_gmm: MixtureConfig = field(default_factory=MixtureConfig)
     depth_gmm: MixtureConfig = field(default_factory=MixtureConfig)
+    augmented_gmm: MixtureConfig = field(default_factory=MixtureConfig)
+    augmented_depth_range: "DepthRescale" = None
     fusion_counter_limit: int = 3
     fusion_initial_label: int = 0
     dilation_radius: int = 1
     warmup_frames: int = 30
+
+    def __post_init__(self):
+        if self.augmented_depth_range is None:
+            self.augmented_depth_range = DepthRescale()
 
     @staticmethod
     def defaults() -> "RunConfig":
@@ -127,6 +133,9 @@ class RunConfig:
         return json.dumps({
             "color_gmm": self.color_gmm.to_dict(),
             "depth_gmm": self.depth_gmm.to_dict(),
+            "augmented_gmm": self.augmented_gmm.to_dict(),
+            "augmented_depth_range": {"min_mm": self.augmented_depth_range.min_mm,
+                                      "max_mm": self.augmented_depth_range.max_mm},
             "fusion": {"counter_limit": self.fusion_counter_limit,
                        "initial_label": self.fusion_initial_label},
             "registration": {"dilation_radius": self.dilation_radius},

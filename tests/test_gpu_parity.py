@@ -722,3 +722,80 @@ def test_planar_single_chunk_host_frames(R, cuda, w, h, S):
         b.process(fr["r"], fr["g"], fr["b"], fr["depth"], want=(), out={"fused": fb})
         assert np.array_equal(np.asarray(fa).reshape(S, h, w), fb.cpu().numpy()), f
     assert a.color_bank().state_equals(b.color_bank())
+
+
+# ------------------------------------------------------------ I/O edge
+
+def test_custom_spec_render_matches_reference_renderer(R, ref, tmp_path):
+    """rgbdseg_render_frame with a JSON spec (two objects, shadows, flicker)
+    against the reference's parse_scenario_spec + render_frame."""
+    import json as _json
+
+    from paper_2110_14934_b200 import synthetic as S
+
+    spec = {"name": "t", "width": 120, "height": 90, "frame_count": 30, "seed": 3,
+            "objects": [{"width": 10, "height": 12, "depth_offset_mm": 300, "color": [10, 200, 30],
+                         "waypoints": [{"frame": 0, "x": 2.5, "y": 3}, {"frame": 29, "x": 100, "y": 70}]},
+                        {"width": 20, "height": 8, "depth_offset_mm": 500,
+                         "waypoints": [{"frame": 0, "x": 60, "y": 40}, {"frame": 10, "x": 61.5, "y": 41},
+                                       {"frame": 29, "x": 5, "y": 5}]}],
+            "illumination": [{"start": 3, "end": 9, "gain": 1.3}],
+            "shadows": [{"start": 5, "end": 20, "region": {"x": 10, "y": 10, "w": 50, "h": 40}},
+                        {"start": 8, "end": 12, "region": {"x": 30, "y": 20, "w": 50, "h": 40}, "darken": 0.5}],
+            "flicker": [{"start": 0, "end": 30, "region": {"x": 70, "y": 0, "w": 50, "h": 30},
+                         "color_sigma": 5.0, "depth_sigma_mm": 20.0}],
+            "noise": {"color_sigma": 2.0, "depth_sigma_mm": 3.0}}
+    path = tmp_path / "spec.json"
+    path.write_text(_json.dumps(spec))
+    s = S.parse_scenario_spec(path)
+    import ctypes as C
+
+    ref.lib.rref_scene_from_json.restype = C.c_void_p
+    ref.lib.rref_scene_from_json.argtypes = [C.c_char_p]
+    h = ref.lib.rref_scene_from_json(str(path).encode())
+    assert h
+    bad = total = 0
+    for f in range(30):
+        d = S.render_frame(s, f)
+        want = {k: np.empty((90, 120), np.uint16 if k == "depth" else np.uint8)
+                for k in ("r", "g", "b", "depth", "gt")}
+        ref.check(ref.lib.rref_render(h, f, want["r"], want["g"], want["b"], want["depth"],
+                                      want["gt"].ctypes.data))
+        for k, v in want.items():
+            bad += int((to_np(d[k][0]) != v).sum())
+            total += v.size
+    ref.lib.rref_scene_destroy(h)
+    assert bad <= total * 1e-5, (bad, total)
+
+
+def test_segment_sequence_end_to_end(R, port, tmp_path):
+    """tests/python/test_smoke.py:76-105 on the GPU path: generate a tiny
+    scenario from a spec, segment it through the pipelined driver, F1 > 0.9
+    at frame 40 -- and every written mask equals the oracle on the decoded
+    PNG frames; pipelined and sequential runs write identical files."""
+    import json as _json
+
+    spec = {"name": "tiny", "width": 64, "height": 48, "frame_count": 50, "seed": 5,
+            "objects": [{"width": 10, "height": 10, "depth_offset_mm": 400,
+                         "waypoints": [{"frame": 0, "x": 5, "y": 5}, {"frame": 49, "x": 40, "y": 30}]}]}
+    sp = tmp_path / "spec.json"
+    sp.write_text(_json.dumps(spec))
+    manifest = R.generate_scenario_from_spec(sp, tmp_path / "seq")
+    stats = R.segment_sequence(manifest, ["fused", "augmented"], tmp_path / "masks", workers=2)
+    assert stats["frames_processed"] == 50
+    fused = R.load_mask_png(tmp_path / "masks" / "fused" / "000040.png")
+    gt = R.load_mask_png(tmp_path / "seq" / "gt" / "000040.png")
+    tp, fp, tn, fn = R.confusion_counts(fused, gt)
+    assert R.f1_score(tp, fp, fn) > 0.9
+    R.segment_sequence(manifest, ["fused"], tmp_path / "seq_masks", pipeline=False)
+    m = R.load_manifest(manifest)
+    orc = O.PortProcessor(port, 64 * 48, O.color_cfg(3), O.depth_cfg(3))
+    for f in range(50):
+        fr = R.load_frame(m, f)
+        rgb, dep, fu = orc.process(fr.r, fr.g, fr.b, fr.depth)
+        name = f"{f:06d}.png"
+        for sub, want in (("rgb", rgb), ("depth", dep), ("fused", fu)):
+            got = R.load_mask_png(tmp_path / "masks" / sub / name)
+            assert np.array_equal(got.ravel(), want), (f, sub)
+        assert np.array_equal(R.load_mask_png(tmp_path / "seq_masks" / "fused" / name).ravel(), fu)
+    assert (tmp_path / "masks" / "augmented" / "000049.png").exists()
