@@ -71,6 +71,24 @@ class ProcessorCfg(C.Structure):
     ]
 
 
+class SceneFrameC(C.Structure):
+    """rgbdseg_scene_frame: one frame of a ScenarioSpec, resolved on the host."""
+
+    _fields_ = [
+        ("width", C.c_int), ("height", C.c_int), ("streams", C.c_int),
+        ("seed0", C.c_uint64), ("frame", C.c_int),
+        ("base_depth_mm", C.c_int), ("depth_texture_mm", C.c_int), ("color_texture", C.c_int),
+        ("gain", C.c_double),
+        ("n_obj", C.c_int), ("obj_rect", (C.c_int * 4) * 4), ("obj_color", (C.c_int * 3) * 4),
+        ("obj_depth_offset_mm", C.c_int * 4),
+        ("n_shadow", C.c_int), ("shadow_rect", (C.c_int * 4) * 16),
+        ("shadow_darken", C.c_double * 16),
+        ("n_flicker", C.c_int), ("flicker_rect", (C.c_int * 4) * 16),
+        ("flicker_color_sigma", C.c_double * 16), ("flicker_depth_sigma_mm", C.c_double * 16),
+        ("noise_color_sigma", C.c_double), ("noise_depth_sigma_mm", C.c_double),
+    ]
+
+
 # Every symbol include/rgbdseg_c.h declares: (restype, argtypes)
 _vp, _sz, _i, _u8 = C.c_void_p, C.c_size_t, C.c_int, C.c_uint8
 SIGNATURES = {
@@ -118,6 +136,7 @@ SIGNATURES = {
     "rgbdseg_processor_set_variant": (_i, [_vp, _i]),
     "rgbdseg_render_scenario": (_i, [C.c_char, _i, _i, _i, C.c_uint64, _i, _vp, _vp, _vp, _vp,
                                      _vp, _i, _vp]),
+    "rgbdseg_render_frame": (_i, [C.POINTER(SceneFrameC), _vp, _vp, _vp, _vp, _vp, _i, _vp]),
 }
 
 

@@ -252,25 +252,7 @@ def scenario_spec_json(spec: ScenarioSpec) -> str:
     }, indent=2)
 
 
-class SceneFrameC(C.Structure):
-    _fields_ = [
-        ("width", C.c_int), ("height", C.c_int), ("streams", C.c_int),
-        ("seed0", C.c_uint64), ("frame", C.c_int),
-        ("base_depth_mm", C.c_int), ("depth_texture_mm", C.c_int), ("color_texture", C.c_int),
-        ("gain", C.c_double),
-        ("n_obj", C.c_int), ("obj_rect", (C.c_int * 4) * 4), ("obj_color", (C.c_int * 3) * 4),
-        ("obj_depth_offset_mm", C.c_int * 4),
-        ("n_shadow", C.c_int), ("shadow_rect", (C.c_int * 4) * 16),
-        ("shadow_darken", C.c_double * 16),
-        ("n_flicker", C.c_int), ("flicker_rect", (C.c_int * 4) * 16),
-        ("flicker_color_sigma", C.c_double * 16), ("flicker_depth_sigma_mm", C.c_double * 16),
-        ("noise_color_sigma", C.c_double), ("noise_depth_sigma_mm", C.c_double),
-    ]
-
-
-lib.rgbdseg_render_frame.restype = C.c_int
-lib.rgbdseg_render_frame.argtypes = [C.POINTER(SceneFrameC)] + [C.c_void_p] * 5 + [C.c_int,
-                                                                                 C.c_void_p]
+SceneFrameC = _lib.SceneFrameC
 
 
 def resolve_frame(spec: ScenarioSpec, frame: int, streams: int = 1,
@@ -337,5 +319,3 @@ def render_frame(spec: ScenarioSpec, frame: int, streams: int = 1, seed0: Option
           "render_frame")
     return out
 
-
-_ = _lib  # keep the module-level library import explicit
