@@ -799,3 +799,21 @@ def test_segment_sequence_end_to_end(R, port, tmp_path):
             assert np.array_equal(got.ravel(), want), (f, sub)
         assert np.array_equal(R.load_mask_png(tmp_path / "seq_masks" / "fused" / name).ravel(), fu)
     assert (tmp_path / "masks" / "augmented" / "000049.png").exists()
+
+
+@pytest.mark.parametrize("limit", [1, 2, 127, 128, 200])
+def test_fusion_counter_limits_int8(R, port, limit):
+    """counter_limit is validated only as >= 1 (fusion.cpp:8) while cpt is
+    int8 (fusion.hpp:13): limits above 127 never saturate and the counter
+    wraps; the GPU mirrors the reference's int8 arithmetic exactly."""
+    rng = np.random.default_rng(limit)
+    n = 4096
+    fs = R.FusionState(n, 1, initial_label=1, counter_limit=limit)
+    out, cpt = np.ones(n, np.uint8), np.zeros(n, np.int8)
+    for step in range(400):
+        r = (rng.random(n) < 0.5).astype(np.uint8)
+        d = (rng.random(n) < (0.9 if step % 50 < 40 else 0.1)).astype(np.uint8)
+        got = fs.step(r.reshape(1, -1), d.reshape(1, -1))
+        port.lib.orc_fuse(out, cpt, n, limit, r, d)
+        assert np.array_equal(got.ravel(), out), step
+        assert np.array_equal(fs.cpt.ravel(), cpt), step
