@@ -16,6 +16,7 @@
 // Built with -fmad=false -prec-div=true -prec-sqrt=true -ftz=false and the
 // arithmetic spelled with explicit _rn intrinsics (gmm_pixel.cuh).
 #include <atomic>
+#include <cstdlib>
 #include <cstdio>
 
 #include "rgbdseg_kernels.cuh"
@@ -294,6 +295,21 @@ __global__ void __launch_bounds__(kThreads, RGBDSEG_FUSED_MIN_BLOCKS(kElide))
     k_fused_ldg(const __grid_constant__ FusedArgs a) {
     const size_t i = (size_t)blockIdx.x * kThreads + threadIdx.x;
     const bool active = i < a.n;
+    if (a.ahead && (threadIdx.x & 31) == 0) {
+        // One bulk L2 prefetch per bank of the warp that starts about one
+        // occupancy wave later: tiled blocks are contiguous, so its whole
+        // state is two contiguous ranges.
+        const size_t ia = i + (size_t)a.ahead * kThreads;
+        if (ia < a.n) {
+            const size_t ja = a.base + ia;
+            const float* ct = a.color.state + (ja / kBlockPx) * bank_stride(MC, 3);
+            const float* dt = a.depth.state + (ja / kBlockPx) * bank_stride(MD, 1);
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ct),
+                         "r"((unsigned)(bank_stride(MC, 3) * 4)));
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(dt),
+                         "r"((unsigned)(bank_stride(MD, 1) * 4)));
+        }
+    }
     uint32_t lab[3] = {0u, 0u, 0u};
     if (active) fused_pixel<MC, MD, kElide>(a, i, lab);
     if (a.gt) {  // evaluation epilogue: the masks never leave registers
@@ -670,8 +686,22 @@ cudaError_t fused_ldg_md(const FusedArgs& a, bool elide, cudaStream_t s) {
 }
 
 template <int MC, int MD>
-cudaError_t fused_md(const FusedArgs& a, int variant, cudaStream_t s) {
-    return fused_ldg_md<MC, MD>(a, variant != kLdgDense, s);
+cudaError_t fused_md(const FusedArgs& a0, int variant, cudaStream_t s) {
+    const bool elide = variant != kLdgDense;
+    static int wave[2] = {-1, -1};  // resident blocks on the device (per variant)
+    int& wv = wave[elide ? 1 : 0];
+    if (wv < 0) {
+        int bps = 0, dev = 0, sms = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &bps, elide ? k_fused_ldg<MC, MD, true> : k_fused_ldg<MC, MD, false>, kThreads, 0);
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        wv = bps * sms;
+        if (const char* e = getenv("RGBDSEG_L2_AHEAD")) wv = atoi(e);  // 0 disables
+    }
+    FusedArgs a = a0;
+    a.ahead = (unsigned)wv;
+    return fused_ldg_md<MC, MD>(a, elide, s);
 }
 
 template <int MC>

@@ -61,6 +61,9 @@ struct FusedArgs {
     const uint8_t* gt;
     unsigned long long* counts;
     size_t stream_px;
+    // L2 prefetch distance in thread blocks (0 = off): each warp prefetches
+    // the bank tiles of the warp `ahead` blocks later (~one occupancy wave)
+    unsigned ahead;
 };
 
 // Kernel variants of K1 (identical results; they differ in HBM writes).
