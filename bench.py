@@ -226,6 +226,9 @@ def main():
     ap.add_argument("--variant", default="auto",
                     choices=["auto", "ldg", "ldg_elide"])
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps")
+    ap.add_argument("--preroll", type=int, default=START_FRAME,
+                    help="untimed frames START_FRAME-P..START_FRAME-1 run first, so the "
+                         "timed frames see a bank in mid-sequence state (default: from frame 0)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-streams", type=int, default=4)
@@ -301,6 +304,18 @@ def main():
         fr = frames[f]
         proc.submit(fr["r"], fr["g"], fr["b"], fr["depth"])
 
+    # ---- pre-roll: the sequence's earlier frames, rendered one at a time ------
+    for f in range(START_FRAME - args.preroll, START_FRAME):
+        if shard == "rows":
+            full = R.render_scenario("A", W, H, f, streams=1, seed0=seed0, device=local)
+            fr = {k: v[:, row0:row0 + my_h].contiguous() for k, v in full.items()}
+            del full
+        else:
+            fr = R.render_scenario("A", W, H, f, streams=my_streams, seed0=seed0, device=local)
+        torch.cuda.current_stream(dev).synchronize()
+        proc.submit(fr["r"], fr["g"], fr["b"], fr["depth"])
+        proc.sync()
+        del fr
     for f in range(args.warmup):
         step(f)
     # ---- timed region: kernel-only, frames in HBM ----------------------------
@@ -441,6 +456,8 @@ def main():
             "config": {"workload": name, "description": text, "width": W, "height": H,
                        "streams": S, "components_color": M, "components_depth": M,
                        "scenario": "A", "frames": f"{START_FRAME}..{START_FRAME + nframes - 1}",
+                       "preroll": (f"frames {START_FRAME - args.preroll}..{START_FRAME - 1} "
+                                   "untimed" if args.preroll else "none (fresh banks)"),
                        "pixels_per_step": total_units, "variant": args.variant,
                        "parallelism": f"{shard}-sharded x{world}",
                        "l2": ("flushed between steps (4x L2 buffer), per-step kernel events summed"

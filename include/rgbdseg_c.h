@@ -97,7 +97,7 @@ int rgbdseg_step_mixtures(rgbdseg_pixel_mixture* mix, const float* values, int c
  * (segmenter.hpp:51-54): mean(i,c) = i*C + c ; variance(i) = M*C + i ;
  * weight(i) = M*C + M + i ; the initialised-flag plane (uint8) is
  * RGBDSEG_FLAGS_PLANE.  In HBM the planes are TILED: blocks of 32 pixels,
- * each holding the 32 values of every plane in turn, then the 32 flag bytes
+ * each holding the 32 values of every plane in turn, then the 32 flag words
  * in a 128-byte slot -- see rgbdseg_bank_device_ptrs. */
 #define RGBDSEG_FLAGS_PLANE (-1)
 int rgbdseg_bank_create(int width, int height, int streams, int mode,
@@ -112,7 +112,12 @@ int rgbdseg_bank_download(const rgbdseg_bank* bank, int plane, void* dst);
 int rgbdseg_bank_upload(rgbdseg_bank* bank, int plane, const void* src);
 /* Raw tiled storage: `nblocks` blocks of `block_bytes` = (planes+1)*128
  * bytes; value of plane p for pixel j is float[(j/32)*(block_bytes/4) +
- * p*32 + j%32], its flag byte is at float offset planes*32 of the block. */
+ * p*32 + j%32]; its flag word is uint16 j%32 from float offset planes*32 of
+ * the block: low byte = initialised flag, high byte = untouched-component
+ * mask (bit i: component i still holds its init_mixture values, mean 0,
+ * variance initial_sigma^2 of the bank's creation cfg, weight 0; the kernels
+ * then skip reading it).  A caller that writes planes through this pointer
+ * must clear the high byte of the pixels it changes. */
 int rgbdseg_bank_device_ptrs(const rgbdseg_bank* bank, void** tiles, size_t* block_bytes,
                              size_t* nblocks);
 

@@ -176,7 +176,20 @@ struct rgbdseg_bank {
     float* state = nullptr;  // tiled: nblocks * bank_stride(M, C) floats
     cudaStream_t stream = nullptr;
     Scratch s_r, s_g, s_b, s_mask, s_plane;
-    BankView view() const { return BankView{state, M, C}; }
+    float vvar = 0.0f;  // sigma0^2 of the creation cfg: an untouched component's variance
+    // Layout view; with a call's cfg it also says whether that call's
+    // init_mixture may mark components untouched (same sigma0^2, and the
+    // fast step's variance range, gmm_pixel.cuh kVarLo/kVarHi).
+    BankView view() const { return BankView{state, M, C, vvar, 0}; }
+    BankView view(const rgbdseg_mixture_cfg& c) const {
+        BankView v = view();
+        uint32_t vb, cb;
+        const float var0 = c.initial_sigma * c.initial_sigma;
+        std::memcpy(&vb, &vvar, 4);
+        std::memcpy(&cb, &var0, 4);
+        v.vinit = vb == cb && vb >= kVarLo && vb < kVarHi;
+        return v;
+    }
 };
 
 struct rgbdseg_fusion {
@@ -322,6 +335,7 @@ int rgbdseg_bank_create(int width, int height, int streams, int mode,
     b->C = mode == RGBDSEG_COLOR3 ? 3 : (mode == RGBDSEG_DEPTH1 ? 1 : 4);
     b->device = device;
     b->cfg = *cfg;
+    b->vvar = cfg->initial_sigma * cfg->initial_sigma;  // k_bank_reset's fmul(sigma0, sigma0)
     b->npx = (size_t)width * height * streams;
     b->nblocks = (b->npx + kBlockPx - 1) / kBlockPx;
     int rc = dalloc(&b->state, b->nblocks * (size_t)bank_stride(b->M, b->C));
@@ -430,7 +444,7 @@ int rgbdseg_segment_color(rgbdseg_bank* b, const uint8_t* r, const uint8_t* g, c
             dm = static_cast<uint8_t*>(p);
         }
     }
-    CU(launch_bank_color(b->view(), to_k(*cfg), (const uint8_t*)dr, (const uint8_t*)dg,
+    CU(launch_bank_color(b->view(*cfg), to_k(*cfg), (const uint8_t*)dr, (const uint8_t*)dg,
                          (const uint8_t*)db, dm, b->npx, b->stream));
     return finish_mask(dm, mask_out, b->npx, b->stream);
 }
@@ -451,7 +465,7 @@ int rgbdseg_segment_depth(rgbdseg_bank* b, const uint16_t* depth_mm,
             dm = static_cast<uint8_t*>(p);
         }
     }
-    CU(launch_bank_depth(b->view(), to_k(*cfg), (const uint16_t*)dd, dm, b->npx, b->stream));
+    CU(launch_bank_depth(b->view(*cfg), to_k(*cfg), (const uint16_t*)dd, dm, b->npx, b->stream));
     return finish_mask(dm, mask_out, b->npx, b->stream);
 }
 
@@ -476,7 +490,7 @@ int rgbdseg_segment_augmented(rgbdseg_bank* b, const uint8_t* r, const uint8_t* 
             dm = static_cast<uint8_t*>(p);
         }
     }
-    CU(launch_bank_aug(b->view(), to_k(*cfg), (const uint8_t*)dr, (const uint8_t*)dg,
+    CU(launch_bank_aug(b->view(*cfg), to_k(*cfg), (const uint8_t*)dr, (const uint8_t*)dg,
                        (const uint8_t*)db, (const uint16_t*)dd, min_mm, max_mm, dm, b->npx,
                        b->stream));
     return finish_mask(dm, mask_out, b->npx, b->stream);
@@ -771,8 +785,8 @@ static int switch_mode(rgbdseg_processor* p, int mode) {
 
 static FusedArgs base_args(const rgbdseg_processor* p) {
     FusedArgs a{};
-    a.color = p->color->view();
-    a.depth = p->depth->view();
+    a.color = p->color->view(p->cfg.color);
+    a.depth = p->depth->view(p->cfg.depth);
     a.ck = to_k(p->cfg.color);
     a.dk = to_k(p->cfg.depth);
     a.limit = p->cfg.fusion_counter_limit;

@@ -47,64 +47,113 @@ template <int M, int C>
 __device__ __forceinline__ float* px_base(const BankView& bk, size_t j) {
     return bk.state + (j / kBlockPx) * bank_stride(M, C) + (j % kBlockPx);
 }
+// Flag word of pixel j: initialised byte | untouched mask << 8.
 template <int M, int C>
-__device__ __forceinline__ uint8_t* px_flag(const BankView& bk, size_t j) {
-    return reinterpret_cast<uint8_t*>(bk.state + (j / kBlockPx) * bank_stride(M, C) +
-                                      bank_planes(M, C) * kBlockPx) +
+__device__ __forceinline__ uint16_t* px_flag(const BankView& bk, size_t j) {
+    return reinterpret_cast<uint16_t*>(bk.state + (j / kBlockPx) * bank_stride(M, C) +
+                                       bank_planes(M, C) * kBlockPx) +
            (j % kBlockPx);
 }
 
-template <int M, int C>
-__device__ __forceinline__ void load_mix(const float* s, Mixture<M, C>& m) {
+// Untouched mask of a loaded flag word (none before initialisation).
+template <int M>
+__device__ __forceinline__ uint32_t flag_untouched(uint32_t f) {
+    return (f & 0xffu) ? (f >> 8) & untouched_all(M) : 0u;
+}
+
+// K of a pixel whose components K..M-1 are untouched and 0..K-1 may not be
+// (the mask is a suffix: a step replaces the weakest component, and every
+// untouched one has fitness +0 and the highest indices, so the first
+// untouched one goes first).  M when the mask is empty or not a suffix.
+template <int M>
+__device__ __forceinline__ int touched_prefix(uint32_t f) {
+    const uint32_t u = flag_untouched<M>(f);
+    const int K = u ? __ffs(u) - 1 : M;
+    return u == (untouched_all(M) & ~((1u << K) - 1u)) ? K : M;
+}
+
+// Flag word after a step on components 0..N-1 (N..M-1 untouched, unchanged).
+// init_mixture (touched < 0) leaves components 1..M-1 at their init values;
+// a step rewrites the touched component, and a weight that is no longer +0
+// (normalisation overflow) also ends "untouched".
+template <int M, int N>
+__device__ __forceinline__ uint32_t flag_after(uint32_t f, int touched, const float (&w)[N],
+                                               const BankView& bk) {
+    if (touched < 0) return 1u | (bk.vinit ? untouched_all(M) << 8 : 0u);
+    uint32_t keep = 0xffffu;
 #pragma unroll
-    for (int i = 0; i < M; ++i)
+    for (int i = 1; i < N; ++i)
+        if (i == touched || __float_as_uint(w[i]) != 0u) keep &= ~(1u << (8 + i));
+    return f & keep;
+}
+
+// Mixture I/O on a bank of layout L components: components 0..N-1 of the
+// pixel at `s` (N <= L).
+template <int L, int N, int C>
+__device__ __forceinline__ void load_mix(const float* s, Mixture<N, C>& m) {
+#pragma unroll
+    for (int i = 0; i < N; ++i)
 #pragma unroll
         for (int c = 0; c < C; ++c) m.mu[i][c] = ld_stream(s + (i * C + c) * kBlockPx);
 #pragma unroll
-    for (int i = 0; i < M; ++i) m.var[i] = ld_stream(s + (M * C + i) * kBlockPx);
+    for (int i = 0; i < N; ++i) m.var[i] = ld_stream(s + (L * C + i) * kBlockPx);
 #pragma unroll
-    for (int i = 0; i < M; ++i) m.w[i] = ld_stream(s + (M * C + M + i) * kBlockPx);
+    for (int i = 0; i < N; ++i) m.w[i] = ld_stream(s + (L * C + L + i) * kBlockPx);
 }
 
-// Dense store of every plane (ModelBank::scatter, segmenter.cpp:49-56).
-template <int M, int C>
-__device__ __forceinline__ void store_mix(float* s, const Mixture<M, C>& m) {
+// load_mix for the components whose bit is set in `need`; the others are
+// untouched (flag word) and take their known values without a memory access.
+template <int L, int N, int C>
+__device__ __forceinline__ void load_mix_need(const float* s, Mixture<N, C>& m, uint32_t need,
+                                              float vvar) {
 #pragma unroll
-    for (int i = 0; i < M; ++i)
+    for (int i = 0; i < N; ++i) {
+        const bool ld = (need >> i) & 1u;
+#pragma unroll
+        for (int c = 0; c < C; ++c) m.mu[i][c] = ld ? ld_stream(s + (i * C + c) * kBlockPx) : 0.0f;
+        m.var[i] = ld ? ld_stream(s + (L * C + i) * kBlockPx) : vvar;
+        m.w[i] = ld ? ld_stream(s + (L * C + L + i) * kBlockPx) : 0.0f;
+    }
+}
+
+// Dense store (ModelBank::scatter, segmenter.cpp:49-56).
+template <int L, int N, int C>
+__device__ __forceinline__ void store_mix(float* s, const Mixture<N, C>& m) {
+#pragma unroll
+    for (int i = 0; i < N; ++i)
 #pragma unroll
         for (int c = 0; c < C; ++c) st_stream(s + (i * C + c) * kBlockPx, m.mu[i][c]);
 #pragma unroll
-    for (int i = 0; i < M; ++i) st_stream(s + (M * C + i) * kBlockPx, m.var[i]);
+    for (int i = 0; i < N; ++i) st_stream(s + (L * C + i) * kBlockPx, m.var[i]);
 #pragma unroll
-    for (int i = 0; i < M; ++i) st_stream(s + (M * C + M + i) * kBlockPx, m.w[i]);
+    for (int i = 0; i < N; ++i) st_stream(s + (L * C + L + i) * kBlockPx, m.w[i]);
 }
 
 // Elided store: identical memory image to store_mix, but words whose bits
 // did not change are not rewritten.  Only the matched / replaced component's
 // mean and variance can change in a step (mixture.cpp:105-113, 125-128); the
-// weights are compared individually.  touched < 0 means "all" (init).
-template <int M, int C>
-__device__ __forceinline__ void store_mix_elide(float* s, const Mixture<M, C>& m, int touched,
-                                                const float (&w_old)[M]) {
+// weights are compared individually.
+template <int L, int N, int C>
+__device__ __forceinline__ void store_mix_elide(float* s, const Mixture<N, C>& m, int touched,
+                                                const float (&w_old)[N]) {
 #pragma unroll
-    for (int i = 0; i < M; ++i) {
-        if (touched < 0 || touched == i) {
+    for (int i = 0; i < N; ++i) {
+        if (touched == i) {
 #pragma unroll
             for (int c = 0; c < C; ++c) st_stream(s + (i * C + c) * kBlockPx, m.mu[i][c]);
-            st_stream(s + (M * C + i) * kBlockPx, m.var[i]);
+            st_stream(s + (L * C + i) * kBlockPx, m.var[i]);
         }
     }
 #pragma unroll
-    for (int i = 0; i < M; ++i)
-        if (touched < 0 || __float_as_uint(m.w[i]) != __float_as_uint(w_old[i]))
-            st_stream(s + (M * C + M + i) * kBlockPx, m.w[i]);
+    for (int i = 0; i < N; ++i)
+        if (__float_as_uint(m.w[i]) != __float_as_uint(w_old[i]))
+            st_stream(s + (L * C + L + i) * kBlockPx, m.w[i]);
 }
 
 // run_bank's per-pixel body (segmenter.cpp:80-96) on a mixture loaded from
-// `src`.  The branch-free fast step runs first; a pixel whose operands leave
-// its exact ranges (gmm_pixel.cuh) is reloaded and replayed by the generic
-// step, so the result is bit-identical either way.  `touched` reports what
-// changed for the elided store.
+// `src` (K1b).  The branch-free fast step runs first; a pixel whose operands
+// leave its exact ranges (gmm_pixel.cuh) is reloaded and replayed by the
+// generic step, so the result is bit-identical either way.
 template <int M, int C>
 __device__ __forceinline__ uint32_t bank_pixel(Mixture<M, C>& m, const float* src,
                                                const float (&v)[C], bool initialised,
@@ -117,10 +166,74 @@ __device__ __forceinline__ uint32_t bank_pixel(Mixture<M, C>& m, const float* sr
     bool ok = k.fast != 0;
     uint32_t label = gmm_step_fast(m, v, k, touched, ok);
     if (!ok) {
-        load_mix(src, m);
+        load_mix<M>(src, m);
         label = gmm_step(m, v, k, touched);
     }
     return label;
+}
+
+// K1's step of one initialised pixel on components 0..N-1 of a bank of M.
+// Components N..M-1 are untouched for this pixel: together with any
+// untouched ones below N they act exactly as the full mixture's untouched
+// tail (fitness +0, ranked after every other component in index order,
+// weight +0 through the update, the same band), so the step on N
+// components returns the full step's label and state.  The elided variant
+// reads only `need`; the dense one (N == M, need = all) rewrites everything.
+template <int M, int C, int N, bool kElide>
+__device__ __forceinline__ uint32_t step_pixel_n(float* s, uint32_t need, const float (&v)[C],
+                                                 const MixCfg& k, const BankView& bk,
+                                                 uint32_t& f) {
+    Mixture<N, C> m;
+    load_mix_need<M>(s, m, need, bk.vvar);
+    float w_old[N];
+#pragma unroll
+    for (int q = 0; q < N; ++q) w_old[q] = m.w[q];
+    int t = 0;
+    bool ok = k.fast != 0;
+    uint32_t label = gmm_step_fast(m, v, k, t, ok);
+    if (ok) {
+        if (kElide)
+            store_mix_elide<M>(s, m, t, w_old);
+        else
+            store_mix<M>(s, m);
+        f = flag_after<M>(f, t, m.w, bk);
+    } else {  // exact replay of the whole mixture from memory
+        Mixture<M, C> mm;
+        load_mix<M>(s, mm);
+        float wo[M];
+#pragma unroll
+        for (int q = 0; q < M; ++q) wo[q] = mm.w[q];
+        label = gmm_step(mm, v, k, t);
+        if (kElide)
+            store_mix_elide<M>(s, mm, t, wo);
+        else
+            store_mix<M>(s, mm);
+        f = flag_after<M>(f, t, mm.w, bk);
+    }
+    return label;
+}
+
+// One K1 bank pixel: init_mixture, or the step on N = min(Kw + 1, M)
+// components where Kw is the warp's largest touched prefix (warp-uniform, so
+// a warp runs one specialisation; the dense variant always takes N = M).
+template <int M, int C, bool kElide>
+__device__ __forceinline__ uint32_t k1_bank_pixel(float* s, uint32_t need, int Kw,
+                                                  const float (&v)[C], const MixCfg& k,
+                                                  const BankView& bk, uint32_t& f) {
+    if (!(f & 0xffu)) {
+        Mixture<M, C> m;
+        gmm_init(m, v, k);
+        store_mix<M>(s, m);
+        f = flag_after<M>(f, -1, m.w, bk);
+        return 0u;
+    }
+    const int N = kElide ? min(Kw + 1, M) : M;
+    if (N <= 2) return step_pixel_n<M, C, 2, kElide>(s, need, v, k, bk, f);
+    if constexpr (M >= 4)
+        if (N == 3) return step_pixel_n<M, C, 3, kElide>(s, need, v, k, bk, f);
+    if constexpr (M >= 5)
+        if (N == 4) return step_pixel_n<M, C, 4, kElide>(s, need, v, k, bk, f);
+    return step_pixel_n<M, C, M, kElide>(s, need, v, k, bk, f);
 }
 
 // ---------------------------------------------------------------- evaluation
@@ -223,55 +336,50 @@ __device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i, uint32
     const uint32_t raw = ld_stream(a.d + i);
     float* cs = px_base<MC, 3>(a.color, j);
     float* ds = px_base<MD, 1>(a.depth, j);
-    uint8_t* cfl = px_flag<MC, 3>(a.color, j);
-    uint8_t* dfl = px_flag<MD, 1>(a.depth, j);
-    const bool cinit = ld_stream(cfl) != 0;
-    const bool dinit = ld_stream(dfl) != 0;
+    uint16_t* cfl = px_flag<MC, 3>(a.color, j);
+    uint16_t* dfl = px_flag<MD, 1>(a.depth, j);
+    const uint32_t cf = ld_stream(cfl);
+    const uint32_t df = ld_stream(dfl);
     const uint32_t out0 = a.fuse ? ld_stream(a.out + i) : 0u;
     const int cpt0 = a.fuse ? (int)ld_stream(a.cpt + i) : 0;
-    Mixture<MC, 3> cm;
-    Mixture<MD, 1> dm;
+    // Components to read: the elided variant skips untouched ones and runs
+    // the step on the warp's touched prefix (+1); the dense one reads all.
+    const uint32_t cneed = kElide ? ~flag_untouched<MC>(cf) : ~0u;
+    const uint32_t dneed = kElide ? ~flag_untouched<MD>(df) : ~0u;
+    const bool dstep = raw != 0 && (df & 0xffu);
+    int kc = MC, kd = MD;
+    if (kElide) {
+        const unsigned am = __activemask();
+        kc = __reduce_max_sync(am, (cf & 0xffu) ? touched_prefix<MC>(cf) : 1);
+        kd = __reduce_max_sync(am, dstep ? touched_prefix<MD>(df) : 1);
+    }
 #if RGBDSEG_PREFETCH_DEPTH
     // The depth mixture goes to L1 now (no registers held) and into registers
     // only after the colour step, lowering the colour step's register peak.
+    if (dstep) {
+        const int nd = min(kd + 1, MD);
 #pragma unroll
-    for (int p = 0; p < bank_planes(MD, 1); ++p)
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(ds + p * kBlockPx));
-    load_mix(cs, cm);
-#else
-    load_mix(cs, cm);
-    load_mix(ds, dm);
+        for (int q = 0; q < MD; ++q)
+            if (q < nd && ((dneed >> q) & 1u)) {
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(ds + q * kBlockPx));
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(ds + (MD + q) * kBlockPx));
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(ds + (2 * MD + q) * kBlockPx));
+            }
+    }
 #endif
 
     // ---- colour stream (segment_color) ----
-    float cw_old[MC];
-#pragma unroll
-    for (int q = 0; q < MC; ++q) cw_old[q] = cm.w[q];
-    int ct = 0;
-    const uint32_t lc = bank_pixel(cm, cs, vc, cinit, a.ck, ct);
-    if (kElide)
-        store_mix_elide(cs, cm, ct, cw_old);
-    else
-        store_mix(cs, cm);
-    if (!cinit) st_stream(cfl, (uint8_t)1);
+    uint32_t cf1 = cf;
+    const uint32_t lc = k1_bank_pixel<MC, 3, kElide>(cs, cneed, kc, vc, a.ck, a.color, cf1);
+    if (cf1 != cf) st_stream(cfl, (uint16_t)cf1);
 
     // ---- depth stream (segment_depth): raw 0 = no return ----
     uint32_t ld = 0;
-#if RGBDSEG_PREFETCH_DEPTH
-    if (raw != 0) load_mix(ds, dm);
-#endif
     if (raw != 0) {
         const float vd[1] = {(float)raw};
-        float dw_old[MD];
-#pragma unroll
-        for (int q = 0; q < MD; ++q) dw_old[q] = dm.w[q];
-        int dt = 0;
-        ld = bank_pixel(dm, ds, vd, dinit, a.dk, dt);
-        if (kElide)
-            store_mix_elide(ds, dm, dt, dw_old);
-        else
-            store_mix(ds, dm);
-        if (!dinit) st_stream(dfl, (uint8_t)1);
+        uint32_t df1 = df;
+        ld = k1_bank_pixel<MD, 1, kElide>(ds, dneed, kd, vd, a.dk, a.depth, df1);
+        if (df1 != df) st_stream(dfl, (uint16_t)df1);
     }
 
     // ---- List-1 fusion on the registered depth mask ----
@@ -328,14 +436,15 @@ __global__ void __launch_bounds__(kThreads)
     if (j >= n) return;
     const float v[3] = {(float)r[j], (float)g[j], (float)b[j]};
     float* st = px_base<M, 3>(bk, j);
-    uint8_t* fl = px_flag<M, 3>(bk, j);
-    const bool init = *fl != 0;
+    uint16_t* fl = px_flag<M, 3>(bk, j);
+    const uint32_t f = *fl;
     Mixture<M, 3> m;
-    load_mix(st, m);
+    load_mix<M>(st, m);
     int t;
-    const uint32_t lab = bank_pixel(m, st, v, init, k, t);
-    store_mix(st, m);
-    if (!init) *fl = 1;
+    const uint32_t lab = bank_pixel(m, st, v, (f & 0xffu) != 0, k, t);
+    store_mix<M>(st, m);
+    const uint32_t f1 = flag_after<M>(f, t, m.w, bk);
+    if (f1 != f) *fl = (uint16_t)f1;
     if (mask) mask[j] = (uint8_t)lab;
 }
 
@@ -350,14 +459,15 @@ __global__ void __launch_bounds__(kThreads)
     if (raw != 0) {  // segmenter.cpp:84,128
         const float v[1] = {(float)raw};
         float* st = px_base<M, 1>(bk, j);
-        uint8_t* fl = px_flag<M, 1>(bk, j);
-        const bool init = *fl != 0;
+        uint16_t* fl = px_flag<M, 1>(bk, j);
+        const uint32_t f = *fl;
         Mixture<M, 1> m;
-        load_mix(st, m);
+        load_mix<M>(st, m);
         int t;
-        lab = bank_pixel(m, st, v, init, k, t);
-        store_mix(st, m);
-        if (!init) *fl = 1;
+        lab = bank_pixel(m, st, v, (f & 0xffu) != 0, k, t);
+        store_mix<M>(st, m);
+        const uint32_t f1 = flag_after<M>(f, t, m.w, bk);
+        if (f1 != f) *fl = (uint16_t)f1;
     }
     if (mask) mask[j] = (uint8_t)lab;
 }
@@ -383,14 +493,15 @@ __global__ void __launch_bounds__(kThreads)
     const float v[4] = {(float)r[j], (float)g[j], (float)b[j],
                         rescale_depth((float)d[j], lo, hi)};
     float* st = px_base<M, 4>(bk, j);
-    uint8_t* fl = px_flag<M, 4>(bk, j);
-    const bool init = *fl != 0;
+    uint16_t* fl = px_flag<M, 4>(bk, j);
+    const uint32_t f = *fl;
     Mixture<M, 4> m;
-    load_mix(st, m);
+    load_mix<M>(st, m);
     int t;
-    const uint32_t lab = bank_pixel(m, st, v, init, k, t);
-    store_mix(st, m);
-    if (!init) *fl = 1;
+    const uint32_t lab = bank_pixel(m, st, v, (f & 0xffu) != 0, k, t);
+    store_mix<M>(st, m);
+    const uint32_t f1 = flag_after<M>(f, t, m.w, bk);
+    if (f1 != f) *fl = (uint16_t)f1;
     if (mask) mask[j] = (uint8_t)lab;
 }
 
@@ -406,7 +517,7 @@ __global__ void k_bank_reset(BankView bk, float sigma0, size_t n) {
         s[(M * C + q) * kBlockPx] = var0;
         s[(M * C + M + q) * kBlockPx] = q == 0 ? 1.0f : 0.0f;
     }
-    reinterpret_cast<uint8_t*>(s - (j % kBlockPx) + NP * kBlockPx)[j % kBlockPx] = 0;
+    reinterpret_cast<uint16_t*>(s - (j % kBlockPx) + NP * kBlockPx)[j % kBlockPx] = 0;
 }
 
 // Flat plane <-> tiled bank (ModelBank::mean_plane / gather / scatter views).
@@ -417,7 +528,7 @@ __global__ void k_bank_gather(BankView bk, int plane, size_t n, void* dst) {
     const float* blk = bk.state + (j / kBlockPx) * bank_stride(bk.M, bk.C);
     if (plane < 0)
         static_cast<uint8_t*>(dst)[j] =
-            reinterpret_cast<const uint8_t*>(blk + NP * kBlockPx)[j % kBlockPx];
+            (uint8_t)reinterpret_cast<const uint16_t*>(blk + NP * kBlockPx)[j % kBlockPx];
     else
         static_cast<float*>(dst)[j] = blk[plane * kBlockPx + j % kBlockPx];
 }
@@ -427,11 +538,13 @@ __global__ void k_bank_scatter(BankView bk, int plane, size_t n, const void* src
     if (j >= n) return;
     const int NP = bank_planes(bk.M, bk.C);
     float* blk = bk.state + (j / kBlockPx) * bank_stride(bk.M, bk.C);
-    if (plane < 0)
-        reinterpret_cast<uint8_t*>(blk + NP * kBlockPx)[j % kBlockPx] =
-            static_cast<const uint8_t*>(src)[j];
-    else
+    uint16_t* fl = reinterpret_cast<uint16_t*>(blk + NP * kBlockPx) + j % kBlockPx;
+    if (plane < 0) {
+        *fl = static_cast<const uint8_t*>(src)[j];  // mask cleared
+    } else {
         blk[plane * kBlockPx + j % kBlockPx] = static_cast<const float*>(src)[j];
+        *fl = *fl & 0xffu;
+    }
 }
 
 // ---------------------------------------------------------------- K1c fusion
@@ -696,7 +809,9 @@ cudaError_t fused_md(const FusedArgs& a0, int variant, cudaStream_t s) {
             &bps, elide ? k_fused_ldg<MC, MD, true> : k_fused_ldg<MC, MD, false>, kThreads, 0);
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        wv = bps * sms;
+        // The elided variant reads only the touched components, so a bulk
+        // prefetch of whole tiles would add the skipped bytes back: off.
+        wv = elide ? 0 : bps * sms;
         if (const char* e = getenv("RGBDSEG_L2_AHEAD")) wv = atoi(e);  // 0 disables
     }
     FusedArgs a = a0;

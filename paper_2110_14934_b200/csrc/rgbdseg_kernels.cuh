@@ -14,7 +14,16 @@ namespace rgbdseg_b200 {
 // in blocks of 32 (one warp); block b stores, for its 32 pixels, float plane
 // 0..NP-1 of ModelBank's plane order (segmenter.hpp:51-54: mean(i,c) = i*C+c,
 // variance(i) = M*C+i, weight(i) = M*C+M+i) as 32 consecutive floats each,
-// then one 128-byte slot whose first 32 bytes are the initialised flags.
+// then one 128-byte slot whose first 64 bytes are the pixels' flag words
+// (uint16): low byte = ModelBank's initialised flag (the value the reference
+// stores), high byte = UNTOUCHED mask, bit i set <=> component i still holds
+// exactly its init_mixture values (mean +0 in every channel, variance =
+// BankView::vvar, weight +0; mixture.cpp:58-72).  The mask is a cache of
+// known state, never a change of it: the planes always hold the full
+// reference state, and K1 substitutes the known values for untouched
+// components instead of reading them (most slots of a mixture are untouched
+// for hundreds of frames).  Every kernel that writes a component clears its
+// bit; upload clears the pixel's mask.
 // A warp's access to one plane is still one full 128-byte line (SoA
 // coalescing), but every plane of a pixel sits at an
 // immediate offset p*128 from one per-thread address, so the kernels issue
@@ -31,7 +40,13 @@ struct BankView {
     float* state;  // nblocks * bank_stride(M, C) floats
     int M;
     int C;
+    float vvar;  // variance of an untouched component: sigma0^2 of the bank's creation cfg
+    int vinit;   // this call's init_mixture may mark components untouched
+                 // (its sigma0^2 == vvar and vvar is in the fast step's range)
 };
+
+// Untouched-mask bits of components 1..M-1 (component 0 is set by init).
+__host__ __device__ constexpr uint32_t untouched_all(int M) { return ((1u << M) - 1u) & ~1u; }
 
 struct FusedArgs {
     // inputs for pixels [0, n) of this launch (pre-offset by the caller)
@@ -81,7 +96,8 @@ cudaError_t launch_bank_aug(BankView bank, const MixCfg& k, const uint8_t* r, co
                             const uint8_t* b, const uint16_t* d, float lo, float hi,
                             uint8_t* mask, size_t n, cudaStream_t s);
 cudaError_t launch_bank_reset(BankView bank, float sigma0, size_t n, cudaStream_t s);
-// plane = ModelBank plane id, or -1 for the flags (uint8).  dst/src: npx elements.
+// plane = ModelBank plane id, or -1 for the initialised flags (uint8).  dst/src:
+// npx elements.  A scatter clears the scattered pixels' untouched masks.
 cudaError_t launch_bank_gather(BankView bank, int plane, size_t n, void* dst, cudaStream_t s);
 cudaError_t launch_bank_scatter(BankView bank, int plane, size_t n, const void* src, cudaStream_t s);
 cudaError_t launch_fuse(uint8_t* out, int8_t* cpt, const uint8_t* rgb, const uint8_t* dep,

@@ -817,3 +817,162 @@ def test_fusion_counter_limits_int8(R, port, limit):
         port.lib.orc_fuse(out, cpt, n, limit, r, d)
         assert np.array_equal(got.ravel(), out), step
         assert np.array_equal(fs.cpt.ravel(), cpt), step
+
+
+# ------------------------------------------------- untouched-component mask
+
+def flag_words(R, bank):
+    """Raw uint16 flag words of a bank (rgbdseg_bank_device_ptrs layout),
+    pixel order: low byte initialised, high byte untouched mask."""
+    import ctypes as C
+
+    import torch
+
+    t, bb, nb = C.c_void_p(), C.c_size_t(), C.c_size_t()
+    R._lib.lib.rgbdseg_bank_device_ptrs(bank._h, C.byref(t), C.byref(bb), C.byref(nb))
+    words = bb.value // 2
+
+    class Raw:
+        __cuda_array_interface__ = {"shape": (nb.value * words,), "typestr": "<u2",
+                                    "data": (t.value, False), "version": 3}
+
+    torch.cuda.synchronize()
+    raw = torch.as_tensor(Raw(), device="cuda").view(torch.int16).cpu().numpy().view(np.uint16)
+    npl = R._lib.lib.rgbdseg_bank_planes(bank._h)
+    blocks = raw.reshape(nb.value, words)[:, npl * 64: npl * 64 + 32]
+    return blocks.reshape(-1)[: bank.npx].copy()
+
+
+def check_untouched_invariant(bank, words, sigma0):
+    """Bit i of a pixel's mask set => component i holds exactly its
+    init_mixture values (mean +0, variance fl(sigma0*sigma0), weight +0)."""
+    M, Ch = bank.components, bank.channels
+    P = bank.planes().reshape(M * Ch + 2 * M, -1)
+    var0 = np.float32(sigma0) * np.float32(sigma0)
+    for i in range(1, M):
+        sel = ((words >> (8 + i)) & 1).astype(bool)
+        for c in range(Ch):
+            assert (P[i * Ch + c][sel].view(np.uint32) == 0).all(), (i, c)
+        assert (P[M * Ch + i][sel] == var0).all(), i
+        assert (P[M * Ch + M + i][sel].view(np.uint32) == 0).all(), i
+    assert not (words >> (8 + M)).any() and not ((words >> 8) & 1).any()
+
+
+@pytest.mark.parametrize("variant", ["auto", "ldg"])
+def test_untouched_mask_set_at_init_and_only_shrinks(R, port, variant):
+    """K1 marks components 1..M-1 untouched when it initialises a pixel
+    (depth: only where a return arrived), clears a component's bit when a
+    step rewrites it, and the marked components always hold their init
+    values; the initialised plane the API returns is the reference's."""
+    w, h, S = 40, 24, 2
+    oc, od = O.color_cfg(5), O.depth_cfg(4)
+    cfg = R.RunConfig.defaults()
+    cfg.color_gmm, cfg.depth_gmm = rcfg(R, oc), rcfg(R, od)
+    proc = R.SequenceProcessor(w, h, cfg, streams=S, variant=variant)
+    ops = [O.PortProcessor(port, w * h, oc, od) for _ in range(S)]
+    sc = [O.PortScene(port, "A", w, h, seed=1 + s) for s in range(S)]
+    prev_c = prev_d = None
+    for f in range(60):
+        frs = [x.render(100 + f) for x in sc]
+        d = np.stack([fr.depth for fr in frs])
+        if f < 4:
+            d[:, :3, :5] = 0  # late first return
+        m = proc.process(*(np.stack([getattr(fr, k) for fr in frs]) for k in "rgb"), d)
+        for s in range(S):
+            rgb, dep, fused = ops[s].process(frs[s].r, frs[s].g, frs[s].b, d[s])
+            assert np.array_equal(m.fused[s].ravel(), fused), (f, s)
+        wc, wd = flag_words(R, proc.color_bank()), flag_words(R, proc.depth_bank())
+        if f == 0:
+            assert (wc == (0x1e << 8 | 1)).all()
+            d0 = d.reshape(-1) != 0
+            assert (wd[d0] == (0x0e << 8 | 1)).all() and (wd[~d0] == 0).all()
+        else:  # bits only clear, except where a pixel initialises now
+            was = (prev_d & 0xff) != 0
+            assert not (wc & ~prev_c & 0xff00).any()
+            assert not (wd[was] & ~prev_d[was] & 0xff00).any()
+            assert (wd[was] & 0xff).all()
+            assert (wd[~was & (wd != 0)] == (0x0e << 8 | 1)).all()
+        prev_c, prev_d = wc, wd
+        if f % 20 == 19:
+            check_untouched_invariant(proc.color_bank(), wc, oc.initial_sigma)
+            check_untouched_invariant(proc.depth_bank(), wd, od.initial_sigma)
+    assert (prev_c >> 8).any() and (prev_d >> 8).any()  # the mask is in use
+    for s in range(S):
+        n = w * h
+        got = proc.color_bank().planes().reshape(-1, S * n)[:, s * n:(s + 1) * n]
+        assert got.tobytes() == ops[s].color.planes().tobytes()
+        got = proc.depth_bank().planes().reshape(-1, S * n)[:, s * n:(s + 1) * n]
+        assert got.tobytes() == ops[s].depth.planes().tobytes()
+
+
+@pytest.mark.parametrize("variant", ["auto", "ldg"])
+def test_upload_and_bank_api_keep_the_mask_exact(R, port, variant):
+    """An uploaded plane (a component written behind K1's back) clears the
+    mask, so the next fused frames read the uploaded words; segment_color on
+    the processor's bank maintains it.  Everything equals the oracle."""
+    rng = np.random.default_rng(5)
+    w, h = 48, 32
+    n = w * h
+    oc, od = O.color_cfg(5), O.depth_cfg(5)
+    cfg = R.RunConfig.defaults()
+    cfg.color_gmm, cfg.depth_gmm = rcfg(R, oc), rcfg(R, od)
+    proc = R.SequenceProcessor(w, h, cfg, variant=variant)
+    op = O.PortProcessor(port, n, oc, od)
+    sc = O.PortScene(port, "A", w, h, seed=3)
+
+    def run(f):
+        fr = sc.render(f)
+        m = proc.process(fr.r, fr.g, fr.b, fr.depth)
+        _, _, fused = op.process(fr.r, fr.g, fr.b, fr.depth)
+        assert np.array_equal(m.fused.ravel(), fused), f
+
+    for f in range(5):
+        run(f)
+    # component 3 of half the pixels becomes a strong, matching component
+    fr = sc.render(5)
+    P = op.color.planes()
+    half = rng.random(n) < 0.5
+    for c, ch in enumerate((fr.r, fr.g, fr.b)):
+        P[3 * 3 + c][half] = ch.ravel()[half].astype(np.float32) + 1.0
+    P[15 + 3][half] = 50.0
+    P[20 + 3][half] = 0.6
+    Pd = op.depth.planes()
+    Pd[4][half] = fr.depth.ravel()[half].astype(np.float32)
+    Pd[5 + 4][half] = 400.0
+    Pd[10 + 4][half] = 0.7
+    for p in (9, 10, 11, 18, 23):
+        proc.color_bank().upload_plane(p, P[p].reshape(h, w))
+    for p in (4, 9, 14):
+        proc.depth_bank().upload_plane(p, Pd[p].reshape(h, w))
+    assert not (flag_words(R, proc.color_bank()) >> 8).any()
+    for f in range(5, 12):
+        run(f)
+    # the single-bank API on the processor's colour bank, then K1 again
+    fr = sc.render(12)
+    m = R.segment_color(proc.color_bank(), fr.r, fr.g, fr.b, cfg.color_gmm)
+    assert np.array_equal(m.ravel(), op.color.segment_color(fr.r, fr.g, fr.b))
+    for f in range(13, 25):
+        run(f)
+    assert proc.color_bank().planes().tobytes() == op.color.planes().tobytes()
+    assert proc.depth_bank().planes().tobytes() == op.depth.planes().tobytes()
+
+
+def test_mask_needs_the_creation_sigma(R, port):
+    """init_mixture marks components untouched only when the call's sigma0
+    is the bank's creation sigma0 (the variance the kernels substitute)."""
+    w, h = 33, 17
+    oc = O.color_cfg(4)
+    other = O.color_cfg(4, initial_sigma=oc.initial_sigma * 0.5)
+    rng = np.random.default_rng(2)
+    for call_cfg, expect in ((oc, 0x0e), (other, 0)):
+        bank = R.ModelBank(w, h, "Color3", rcfg(R, oc))
+        ob = O.PortBank(port, w * h, 3, oc)
+        ob.cfg = call_cfg
+        for f in range(8):
+            r, g, b = (rng.integers(0, 256, (h, w), dtype=np.uint8) for _ in range(3))
+            m = R.segment_color(bank, r, g, b, rcfg(R, call_cfg))
+            assert np.array_equal(m.ravel(), ob.segment_color(r, g, b))
+            if f == 0:
+                assert (flag_words(R, bank) >> 8 == expect).all()
+        assert bank.planes().tobytes() == ob.planes().tobytes()
+        check_untouched_invariant(bank, flag_words(R, bank), oc.initial_sigma)
