@@ -226,9 +226,11 @@ def main():
     ap.add_argument("--variant", default="auto",
                     choices=["auto", "ldg", "ldg_elide"])
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps")
-    ap.add_argument("--preroll", type=int, default=START_FRAME,
-                    help="untimed frames START_FRAME-P..START_FRAME-1 run first, so the "
-                         "timed frames see a bank in mid-sequence state (default: from frame 0)")
+    ap.add_argument("--start", type=int, default=START_FRAME,
+                    help="first warm-up frame of scenario A (timed frames follow the warm-up)")
+    ap.add_argument("--preroll", type=int, default=None,
+                    help="untimed frames start-P..start-1 run first, so the timed frames see "
+                         "a bank in mid-sequence state (default: the whole sequence from 0)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-streams", type=int, default=4)
@@ -283,17 +285,20 @@ def main():
                                variant=args.variant)
     ext = torch.cuda.ExternalStream(proc.stream_handle, device=dev)
 
+    start = args.start
+    if args.preroll is None:
+        args.preroll = start
     # ---- inputs resident in HBM before timing --------------------------------
     nframes = args.warmup + args.steps
     frames = []
     for f in range(nframes):
         if shard == "rows":  # render the full-width frame's row band: render then slice
-            full = R.render_scenario("A", W, H, START_FRAME + f, streams=1, seed0=seed0,
+            full = R.render_scenario("A", W, H, start + f, streams=1, seed0=seed0,
                                      device=local)
             frames.append({k: v[:, row0:row0 + my_h].contiguous() for k, v in full.items()})
             del full
         else:
-            frames.append(R.render_scenario("A", W, H, START_FRAME + f, streams=my_streams,
+            frames.append(R.render_scenario("A", W, H, start + f, streams=my_streams,
                                             seed0=seed0, device=local))
     torch.cuda.synchronize()
     state_bytes = npx * (bytes_per_px(M, M) - 5)
@@ -305,7 +310,7 @@ def main():
         proc.submit(fr["r"], fr["g"], fr["b"], fr["depth"])
 
     # ---- pre-roll: the sequence's earlier frames, rendered one at a time ------
-    for f in range(START_FRAME - args.preroll, START_FRAME):
+    for f in range(start - args.preroll, start):
         if shard == "rows":
             full = R.render_scenario("A", W, H, f, streams=1, seed0=seed0, device=local)
             fr = {k: v[:, row0:row0 + my_h].contiguous() for k, v in full.items()}
@@ -434,8 +439,8 @@ def main():
         cb = cpu_reference(sample_frames, W, my_h, M, M, min_seconds=args.cpu_seconds)
         cpu = {"value": round(cb["value"], 3), "unit": "Mpix/s", "cores": cb["cores"],
                "kind": cb["kind"],
-               "sample": (f"stream 0 ({W}x{my_h}, seed {seed0}) frames {START_FRAME}.."
-                          f"{START_FRAME + len(sample_frames) - 1} cycled, {cb['frames']} "
+               "sample": (f"stream 0 ({W}x{my_h}, seed {seed0}) frames {start}.."
+                          f"{start + len(sample_frames) - 1} cycled, {cb['frames']} "
                           f"frames in {cb['seconds']:.1f} s, SequenceProcessor::process "
                           f"(fused), workers={cb['cores']}")}
 
@@ -455,8 +460,8 @@ def main():
             "data": "synthetic",
             "config": {"workload": name, "description": text, "width": W, "height": H,
                        "streams": S, "components_color": M, "components_depth": M,
-                       "scenario": "A", "frames": f"{START_FRAME}..{START_FRAME + nframes - 1}",
-                       "preroll": (f"frames {START_FRAME - args.preroll}..{START_FRAME - 1} "
+                       "scenario": "A", "frames": f"{start}..{start + nframes - 1}",
+                       "preroll": (f"frames {start - args.preroll}..{start - 1} "
                                    "untimed" if args.preroll else "none (fresh banks)"),
                        "pixels_per_step": total_units, "variant": args.variant,
                        "parallelism": f"{shard}-sharded x{world}",

@@ -179,12 +179,41 @@ __device__ __forceinline__ uint32_t bank_pixel(Mixture<M, C>& m, const float* sr
 // weight +0 through the update, the same band), so the step on N
 // components returns the full step's label and state.  The elided variant
 // reads only `need`; the dense one (N == M, need = all) rewrites everything.
-template <int M, int C, int N, bool kElide>
-__device__ __forceinline__ uint32_t step_pixel_n(float* s, uint32_t need, const float (&v)[C],
+// Exact replay of a pixel the fast step refused: the whole mixture from
+// memory through the generic gmm_step.  Rare, so one out-of-line copy per
+// bank shape instead of one inlined per specialisation (code size).
+template <int M, int C, bool kElide>
+__device__ __noinline__ uint32_t replay_pixel(float* s, const float (&v)[C], const MixCfg& k,
+                                              const BankView& bk, uint32_t& f) {
+    Mixture<M, C> mm;
+    load_mix<M>(s, mm);
+    float wo[M];
+#pragma unroll
+    for (int q = 0; q < M; ++q) wo[q] = mm.w[q];
+    int t = 0;
+    const uint32_t label = gmm_step(mm, v, k, t);
+    if (kElide)
+        store_mix_elide<M>(s, mm, t, wo);
+    else
+        store_mix<M>(s, mm);
+    f = flag_after<M>(f, t, mm.w, bk);
+    return label;
+}
+
+template <int M, int C, int N, int P, bool kElide>
+__device__ __forceinline__ uint32_t step_pixel_n(float* s, const Mixture<(P > 0 ? P : 1), C>& pre,
+                                                 uint32_t need, const float (&v)[C],
                                                  const MixCfg& k, const BankView& bk,
                                                  uint32_t& f) {
     Mixture<N, C> m;
-    load_mix_need<M>(s, m, need, bk.vvar);
+    load_mix_need<M>(s, m, need & ~((1u << P) - 1u), bk.vvar);
+#pragma unroll
+    for (int i = 0; i < (P < N ? P : N); ++i) {  // loaded with the flags (exact values)
+#pragma unroll
+        for (int c = 0; c < C; ++c) m.mu[i][c] = pre.mu[i][c];
+        m.var[i] = pre.var[i];
+        m.w[i] = pre.w[i];
+    }
     float w_old[N];
 #pragma unroll
     for (int q = 0; q < N; ++q) w_old[q] = m.w[q];
@@ -197,18 +226,8 @@ __device__ __forceinline__ uint32_t step_pixel_n(float* s, uint32_t need, const 
         else
             store_mix<M>(s, m);
         f = flag_after<M>(f, t, m.w, bk);
-    } else {  // exact replay of the whole mixture from memory
-        Mixture<M, C> mm;
-        load_mix<M>(s, mm);
-        float wo[M];
-#pragma unroll
-        for (int q = 0; q < M; ++q) wo[q] = mm.w[q];
-        label = gmm_step(mm, v, k, t);
-        if (kElide)
-            store_mix_elide<M>(s, mm, t, wo);
-        else
-            store_mix<M>(s, mm);
-        f = flag_after<M>(f, t, mm.w, bk);
+    } else {
+        label = replay_pixel<M, C, kElide>(s, v, k, bk, f);
     }
     return label;
 }
@@ -216,10 +235,12 @@ __device__ __forceinline__ uint32_t step_pixel_n(float* s, uint32_t need, const 
 // One K1 bank pixel: init_mixture, or the step on N = min(Kw + 1, M)
 // components where Kw is the warp's largest touched prefix (warp-uniform, so
 // a warp runs one specialisation; the dense variant always takes N = M).
-template <int M, int C, bool kElide>
-__device__ __forceinline__ uint32_t k1_bank_pixel(float* s, uint32_t need, int Kw,
-                                                  const float (&v)[C], const MixCfg& k,
-                                                  const BankView& bk, uint32_t& f) {
+// Components 0..P-1 arrive in `pre`, loaded before the flags were known.
+template <int M, int C, int P, bool kElide>
+__device__ __forceinline__ uint32_t k1_bank_pixel(float* s, const Mixture<(P > 0 ? P : 1), C>& pre,
+                                                  uint32_t need, int Kw, const float (&v)[C],
+                                                  const MixCfg& k, const BankView& bk,
+                                                  uint32_t& f) {
     if (!(f & 0xffu)) {
         Mixture<M, C> m;
         gmm_init(m, v, k);
@@ -228,12 +249,12 @@ __device__ __forceinline__ uint32_t k1_bank_pixel(float* s, uint32_t need, int K
         return 0u;
     }
     const int N = kElide ? min(Kw + 1, M) : M;
-    if (N <= 2) return step_pixel_n<M, C, 2, kElide>(s, need, v, k, bk, f);
+    if (N <= 2) return step_pixel_n<M, C, 2, P, kElide>(s, pre, need, v, k, bk, f);
     if constexpr (M >= 4)
-        if (N == 3) return step_pixel_n<M, C, 3, kElide>(s, need, v, k, bk, f);
+        if (N == 3) return step_pixel_n<M, C, 3, P, kElide>(s, pre, need, v, k, bk, f);
     if constexpr (M >= 5)
-        if (N == 4) return step_pixel_n<M, C, 4, kElide>(s, need, v, k, bk, f);
-    return step_pixel_n<M, C, M, kElide>(s, need, v, k, bk, f);
+        if (N == 4) return step_pixel_n<M, C, 4, P, kElide>(s, pre, need, v, k, bk, f);
+    return step_pixel_n<M, C, M, P, kElide>(s, pre, need, v, k, bk, f);
 }
 
 // ---------------------------------------------------------------- evaluation
@@ -322,8 +343,69 @@ __global__ void __launch_bounds__(kThreads)
 #define RGBDSEG_PREFETCH_DEPTH 1
 #endif
 #ifndef RGBDSEG_FUSED_MIN_BLOCKS
-#define RGBDSEG_FUSED_MIN_BLOCKS(elide) ((elide) ? 4 : 3)
+#define RGBDSEG_FUSED_MIN_BLOCKS(elide) ((elide) ? 6 : 3)
 #endif
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// Component of plane p of a bank (mean i*C+c, variance M*C+i, weight M*C+M+i).
+template <int M, int C>
+__device__ __forceinline__ int plane_component(int p) {
+    return p < M * C ? p / C : (p < M * C + M ? p - M * C : p - M * C - M);
+}
+
+// L2 pipeline of the elided K1, run by every warp at its start (a.ahead =
+// resident blocks, ~one wave):
+//  * two waves ahead: the sectors of the warp's first round of loads
+//    (inputs, both flag words, fusion state) -- lanes 0..9, one sector each;
+//  * one wave ahead: that warp's flag words (in L2 by now) give the
+//    components any of its pixels will read; lane p prefetches plane p of
+//    each bank only if it is needed, so untouched planes are never fetched.
+// Prefetches are hints: a warp straddling two tiles (chunk bases not a
+// multiple of 32) just prefetches the first one.
+template <int MC, int MD>
+__device__ __forceinline__ void l2_ahead_elided(const FusedArgs& a, size_t i) {
+    const unsigned lane = threadIdx.x & 31;
+    const size_t w0 = i - lane;
+    const size_t i2 = w0 + 2 * (size_t)a.ahead * kThreads;
+    if (i2 < a.n && lane < 10) {
+        const size_t j2 = a.base + i2;
+        const void* p;
+        switch (lane) {
+            case 0: p = a.r + i2; break;
+            case 1: p = a.g + i2; break;
+            case 2: p = a.b + i2; break;
+            case 3: p = a.d + i2; break;
+            case 4: p = a.d + i2 + 16; break;
+            case 5: p = a.fuse ? (const void*)(a.out + i2) : (const void*)(a.d + i2); break;
+            case 6: p = a.fuse ? (const void*)(a.cpt + i2) : (const void*)(a.d + i2); break;
+            case 7: p = px_flag<MC, 3>(a.color, j2); break;
+            case 8: p = px_flag<MD, 1>(a.depth, j2); break;
+            default: p = px_flag<MC, 3>(a.color, j2) + 16; break;
+        }
+        prefetch_l2(p);
+        if (lane == 9) prefetch_l2(px_flag<MD, 1>(a.depth, j2) + 16);
+    }
+    const size_t i1 = i + (size_t)a.ahead * kThreads;
+    uint32_t cu = 0u, du = 0u;
+    const size_t j1 = a.base + (i1 < a.n ? i1 : 0);
+    if (i1 < a.n) {  // plain loads: the lines stay in L2 for their owner
+        const uint32_t cf = *px_flag<MC, 3>(a.color, j1);
+        const uint32_t df = *px_flag<MD, 1>(a.depth, j1);
+        cu = (cf & 0xffu) ? ~flag_untouched<MC>(cf) & ((1u << MC) - 1u) : 0u;
+        du = (df & 0xffu) ? ~flag_untouched<MD>(df) & ((1u << MD) - 1u) : 0u;
+    }
+    const unsigned am = __activemask();
+    cu = __reduce_or_sync(am, cu);
+    du = __reduce_or_sync(am, du);
+    const size_t jt = __shfl_sync(am, j1, 0) / kBlockPx;
+    if ((int)lane < bank_planes(MC, 3) && ((cu >> plane_component<MC, 3>(lane)) & 1u))
+        prefetch_l2(a.color.state + jt * bank_stride(MC, 3) + lane * kBlockPx);
+    if ((int)lane < bank_planes(MD, 1) && ((du >> plane_component<MD, 1>(lane)) & 1u))
+        prefetch_l2(a.depth.state + jt * bank_stride(MD, 1) + lane * kBlockPx);
+}
+
 // One pixel of K1; returns the three labels for the evaluation epilogue.
 template <int MC, int MD, bool kElide>
 __device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i, uint32_t (&lab)[3]) {
@@ -342,6 +424,20 @@ __device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i, uint32
     const uint32_t df = ld_stream(dfl);
     const uint32_t out0 = a.fuse ? ld_stream(a.out + i) : 0u;
     const int cpt0 = a.fuse ? (int)ld_stream(a.cpt + i) : 0;
+    // First round, independent of the flags: colour components 0..kPreC-1
+    // (component 0 is touched in every initialised pixel and component 1 in
+    // most; a loaded untouched component equals its substitute) and, into
+    // L1, depth component 0.  Only the rest waits for the flag words.
+    constexpr int kPreC = MC > 2 ? 2 : MC;
+    Mixture<kPreC, 3> cpre;
+    load_mix<MC>(cs, cpre);
+#if RGBDSEG_PREFETCH_DEPTH
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(ds));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(ds + MD * kBlockPx));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(ds + 2 * MD * kBlockPx));
+#endif
+    // while this pixel's first round of loads is in flight
+    if (kElide && a.ahead) l2_ahead_elided<MC, MD>(a, i);
     // Components to read: the elided variant skips untouched ones and runs
     // the step on the warp's touched prefix (+1); the dense one reads all.
     const uint32_t cneed = kElide ? ~flag_untouched<MC>(cf) : ~0u;
@@ -359,7 +455,7 @@ __device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i, uint32
     if (dstep) {
         const int nd = min(kd + 1, MD);
 #pragma unroll
-        for (int q = 0; q < MD; ++q)
+        for (int q = 1; q < MD; ++q)
             if (q < nd && ((dneed >> q) & 1u)) {
                 asm volatile("prefetch.global.L1 [%0];" ::"l"(ds + q * kBlockPx));
                 asm volatile("prefetch.global.L1 [%0];" ::"l"(ds + (MD + q) * kBlockPx));
@@ -370,7 +466,7 @@ __device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i, uint32
 
     // ---- colour stream (segment_color) ----
     uint32_t cf1 = cf;
-    const uint32_t lc = k1_bank_pixel<MC, 3, kElide>(cs, cneed, kc, vc, a.ck, a.color, cf1);
+    const uint32_t lc = k1_bank_pixel<MC, 3, kPreC, kElide>(cs, cpre, cneed, kc, vc, a.ck, a.color, cf1);
     if (cf1 != cf) st_stream(cfl, (uint16_t)cf1);
 
     // ---- depth stream (segment_depth): raw 0 = no return ----
@@ -378,7 +474,8 @@ __device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i, uint32
     if (raw != 0) {
         const float vd[1] = {(float)raw};
         uint32_t df1 = df;
-        ld = k1_bank_pixel<MD, 1, kElide>(ds, dneed, kd, vd, a.dk, a.depth, df1);
+        const Mixture<1, 1> none{};
+        ld = k1_bank_pixel<MD, 1, 0, kElide>(ds, none, dneed, kd, vd, a.dk, a.depth, df1);
         if (df1 != df) st_stream(dfl, (uint16_t)df1);
     }
 
@@ -403,7 +500,7 @@ __global__ void __launch_bounds__(kThreads, RGBDSEG_FUSED_MIN_BLOCKS(kElide))
     k_fused_ldg(const __grid_constant__ FusedArgs a) {
     const size_t i = (size_t)blockIdx.x * kThreads + threadIdx.x;
     const bool active = i < a.n;
-    if (a.ahead && (threadIdx.x & 31) == 0) {
+    if (!kElide && a.ahead && (threadIdx.x & 31) == 0) {
         // One bulk L2 prefetch per bank of the warp that starts about one
         // occupancy wave later: tiled blocks are contiguous, so its whole
         // state is two contiguous ranges.
@@ -809,8 +906,8 @@ cudaError_t fused_md(const FusedArgs& a0, int variant, cudaStream_t s) {
             &bps, elide ? k_fused_ldg<MC, MD, true> : k_fused_ldg<MC, MD, false>, kThreads, 0);
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        // The elided variant reads only the touched components, so a bulk
-        // prefetch of whole tiles would add the skipped bytes back: off.
+        // Elided: the flag-aware L2 pipeline (l2_ahead_elided) measured
+        // slower than none (profiles/variants_r01.json), so it is opt-in.
         wv = elide ? 0 : bps * sms;
         if (const char* e = getenv("RGBDSEG_L2_AHEAD")) wv = atoi(e);  // 0 disables
     }
