@@ -342,70 +342,12 @@ __global__ void __launch_bounds__(kThreads)
 #ifndef RGBDSEG_PREFETCH_DEPTH
 #define RGBDSEG_PREFETCH_DEPTH 1
 #endif
+#ifndef RGBDSEG_PRE_COLOR  // colour components loaded with the flag words
+#define RGBDSEG_PRE_COLOR 2
+#endif
 #ifndef RGBDSEG_FUSED_MIN_BLOCKS
 #define RGBDSEG_FUSED_MIN_BLOCKS(elide) ((elide) ? 6 : 3)
 #endif
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
-
-// Component of plane p of a bank (mean i*C+c, variance M*C+i, weight M*C+M+i).
-template <int M, int C>
-__device__ __forceinline__ int plane_component(int p) {
-    return p < M * C ? p / C : (p < M * C + M ? p - M * C : p - M * C - M);
-}
-
-// L2 pipeline of the elided K1, run by every warp at its start (a.ahead =
-// resident blocks, ~one wave):
-//  * two waves ahead: the sectors of the warp's first round of loads
-//    (inputs, both flag words, fusion state) -- lanes 0..9, one sector each;
-//  * one wave ahead: that warp's flag words (in L2 by now) give the
-//    components any of its pixels will read; lane p prefetches plane p of
-//    each bank only if it is needed, so untouched planes are never fetched.
-// Prefetches are hints: a warp straddling two tiles (chunk bases not a
-// multiple of 32) just prefetches the first one.
-template <int MC, int MD>
-__device__ __forceinline__ void l2_ahead_elided(const FusedArgs& a, size_t i) {
-    const unsigned lane = threadIdx.x & 31;
-    const size_t w0 = i - lane;
-    const size_t i2 = w0 + 2 * (size_t)a.ahead * kThreads;
-    if (i2 < a.n && lane < 10) {
-        const size_t j2 = a.base + i2;
-        const void* p;
-        switch (lane) {
-            case 0: p = a.r + i2; break;
-            case 1: p = a.g + i2; break;
-            case 2: p = a.b + i2; break;
-            case 3: p = a.d + i2; break;
-            case 4: p = a.d + i2 + 16; break;
-            case 5: p = a.fuse ? (const void*)(a.out + i2) : (const void*)(a.d + i2); break;
-            case 6: p = a.fuse ? (const void*)(a.cpt + i2) : (const void*)(a.d + i2); break;
-            case 7: p = px_flag<MC, 3>(a.color, j2); break;
-            case 8: p = px_flag<MD, 1>(a.depth, j2); break;
-            default: p = px_flag<MC, 3>(a.color, j2) + 16; break;
-        }
-        prefetch_l2(p);
-        if (lane == 9) prefetch_l2(px_flag<MD, 1>(a.depth, j2) + 16);
-    }
-    const size_t i1 = i + (size_t)a.ahead * kThreads;
-    uint32_t cu = 0u, du = 0u;
-    const size_t j1 = a.base + (i1 < a.n ? i1 : 0);
-    if (i1 < a.n) {  // plain loads: the lines stay in L2 for their owner
-        const uint32_t cf = *px_flag<MC, 3>(a.color, j1);
-        const uint32_t df = *px_flag<MD, 1>(a.depth, j1);
-        cu = (cf & 0xffu) ? ~flag_untouched<MC>(cf) & ((1u << MC) - 1u) : 0u;
-        du = (df & 0xffu) ? ~flag_untouched<MD>(df) & ((1u << MD) - 1u) : 0u;
-    }
-    const unsigned am = __activemask();
-    cu = __reduce_or_sync(am, cu);
-    du = __reduce_or_sync(am, du);
-    const size_t jt = __shfl_sync(am, j1, 0) / kBlockPx;
-    if ((int)lane < bank_planes(MC, 3) && ((cu >> plane_component<MC, 3>(lane)) & 1u))
-        prefetch_l2(a.color.state + jt * bank_stride(MC, 3) + lane * kBlockPx);
-    if ((int)lane < bank_planes(MD, 1) && ((du >> plane_component<MD, 1>(lane)) & 1u))
-        prefetch_l2(a.depth.state + jt * bank_stride(MD, 1) + lane * kBlockPx);
-}
-
 // One pixel of K1; returns the three labels for the evaluation epilogue.
 template <int MC, int MD, bool kElide>
 __device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i, uint32_t (&lab)[3]) {
@@ -428,7 +370,7 @@ __device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i, uint32
     // (component 0 is touched in every initialised pixel and component 1 in
     // most; a loaded untouched component equals its substitute) and, into
     // L1, depth component 0.  Only the rest waits for the flag words.
-    constexpr int kPreC = MC > 2 ? 2 : MC;
+    constexpr int kPreC = MC > RGBDSEG_PRE_COLOR ? RGBDSEG_PRE_COLOR : MC;
     Mixture<kPreC, 3> cpre;
     load_mix<MC>(cs, cpre);
 #if RGBDSEG_PREFETCH_DEPTH
@@ -436,8 +378,6 @@ __device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i, uint32
     asm volatile("prefetch.global.L1 [%0];" ::"l"(ds + MD * kBlockPx));
     asm volatile("prefetch.global.L1 [%0];" ::"l"(ds + 2 * MD * kBlockPx));
 #endif
-    // while this pixel's first round of loads is in flight
-    if (kElide && a.ahead) l2_ahead_elided<MC, MD>(a, i);
     // Components to read: the elided variant skips untouched ones and runs
     // the step on the warp's touched prefix (+1); the dense one reads all.
     const uint32_t cneed = kElide ? ~flag_untouched<MC>(cf) : ~0u;
@@ -906,8 +846,9 @@ cudaError_t fused_md(const FusedArgs& a0, int variant, cudaStream_t s) {
             &bps, elide ? k_fused_ldg<MC, MD, true> : k_fused_ldg<MC, MD, false>, kThreads, 0);
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        // Elided: the flag-aware L2 pipeline (l2_ahead_elided) measured
-        // slower than none (profiles/variants_r01.json), so it is opt-in.
+        // The elided kernel reads only what its flags ask for; every L2
+        // prefetch tried ahead of it (whole tiles, first-round lines, flag-
+        // aware planes) measured slower (profiles/variants_r01.json): off.
         wv = elide ? 0 : bps * sms;
         if (const char* e = getenv("RGBDSEG_L2_AHEAD")) wv = atoi(e);  // 0 disables
     }
