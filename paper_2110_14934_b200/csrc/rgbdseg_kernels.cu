@@ -68,8 +68,8 @@ __device__ __forceinline__ uint32_t flag_untouched(uint32_t f) {
 template <int M>
 __device__ __forceinline__ int touched_prefix(uint32_t f) {
     const uint32_t u = flag_untouched<M>(f);
-    const int K = u ? __ffs(u) - 1 : M;
-    return u == (untouched_all(M) & ~((1u << K) - 1u)) ? K : M;
+    const int K = M - __popc(u);  // a suffix of |u| bits starts at K
+    return u == (1u << M) - (1u << K) ? K : M;
 }
 
 // Flag word after a step on components 0..N-1 (N..M-1 untouched, unchanged).
@@ -348,24 +348,33 @@ __global__ void __launch_bounds__(kThreads)
 #ifndef RGBDSEG_FUSED_MIN_BLOCKS
 #define RGBDSEG_FUSED_MIN_BLOCKS(elide) ((elide) ? 6 : 3)
 #endif
-// One pixel of K1; returns the three labels for the evaluation epilogue.
+// One pixel of K1 (thread t of the block whose first pixel is i0); returns
+// the three labels for the evaluation epilogue.  Addresses are a per-block
+// uniform base plus a 32-bit per-thread offset: tiles are warp-aligned
+// (launch_fused requires base % 32 == 0), so warp w of the block owns tile
+// (base + i0) / 32 + w.
 template <int MC, int MD, bool kElide>
-__device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i, uint32_t (&lab)[3]) {
-    const size_t j = a.base + i;
+__device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i0, unsigned t,
+                                            uint32_t (&lab)[3]) {
+    constexpr unsigned SC = bank_stride(MC, 3), SD = bank_stride(MD, 1);
+    const size_t tile0 = (a.base + i0) / kBlockPx;
+    const unsigned w = t / kBlockPx, lane = t % kBlockPx;
+    float* cs = a.color.state + tile0 * SC + (w * SC + lane);
+    float* ds = a.depth.state + tile0 * SD + (w * SD + lane);
+    uint16_t* cfl = reinterpret_cast<uint16_t*>(a.color.state + tile0 * SC + bank_planes(MC, 3) * kBlockPx) +
+                    (w * SC * 2 + lane);
+    uint16_t* dfl = reinterpret_cast<uint16_t*>(a.depth.state + tile0 * SD + bank_planes(MD, 1) * kBlockPx) +
+                    (w * SD * 2 + lane);
 
-    // Issue every load of the pixel before any math: inputs, flags, fusion
-    // state and both mixtures (40 planes at M=5) are independent requests.
-    const float vc[3] = {(float)ld_stream(a.r + i), (float)ld_stream(a.g + i),
-                         (float)ld_stream(a.b + i)};
-    const uint32_t raw = ld_stream(a.d + i);
-    float* cs = px_base<MC, 3>(a.color, j);
-    float* ds = px_base<MD, 1>(a.depth, j);
-    uint16_t* cfl = px_flag<MC, 3>(a.color, j);
-    uint16_t* dfl = px_flag<MD, 1>(a.depth, j);
+    // Issue every load that does not depend on the flags first: inputs,
+    // flags, fusion state, the first colour components.
+    const float vc[3] = {(float)ld_stream(a.r + i0 + t), (float)ld_stream(a.g + i0 + t),
+                         (float)ld_stream(a.b + i0 + t)};
+    const uint32_t raw = ld_stream(a.d + i0 + t);
     const uint32_t cf = ld_stream(cfl);
     const uint32_t df = ld_stream(dfl);
-    const uint32_t out0 = a.fuse ? ld_stream(a.out + i) : 0u;
-    const int cpt0 = a.fuse ? (int)ld_stream(a.cpt + i) : 0;
+    const uint32_t out0 = a.fuse ? ld_stream(a.out + i0 + t) : 0u;
+    const int cpt0 = a.fuse ? (int)ld_stream(a.cpt + i0 + t) : 0;
     // First round, independent of the flags: colour components 0..kPreC-1
     // (component 0 is touched in every initialised pixel and component 1 in
     // most; a loaded untouched component equals its substitute) and, into
@@ -390,9 +399,10 @@ __device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i, uint32
         kd = __reduce_max_sync(am, dstep ? touched_prefix<MD>(df) : 1);
     }
 #if RGBDSEG_PREFETCH_DEPTH
-    // The depth mixture goes to L1 now (no registers held) and into registers
-    // only after the colour step, lowering the colour step's register peak.
-    if (dstep) {
+    // The rest of the depth mixture goes to L1 now (no registers held) and
+    // into registers only after the colour step.  Only warps with a touched
+    // depth component 1 have any.
+    if (kd >= 2 && dstep) {
         const int nd = min(kd + 1, MD);
 #pragma unroll
         for (int q = 1; q < MD; ++q)
@@ -424,12 +434,12 @@ __device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i, uint32
     int cpt = cpt0;
     if (a.fuse) {
         fuse_pixel(lc, ld, a.limit, out, cpt);
-        if (!kElide || out != out0) st_stream(a.out + i, (uint8_t)out);
-        if (!kElide || cpt != cpt0) st_stream(a.cpt + i, (int8_t)cpt);
+        if (!kElide || out != out0) st_stream(a.out + i0 + t, (uint8_t)out);
+        if (!kElide || cpt != cpt0) st_stream(a.cpt + i0 + t, (int8_t)cpt);
     }
-    if (a.rgb_mask) st_stream(a.rgb_mask + i, (uint8_t)lc);
-    if (a.depth_mask) st_stream(a.depth_mask + i, (uint8_t)ld);
-    if (a.fused_copy) st_stream(a.fused_copy + i, (uint8_t)out);
+    if (a.rgb_mask) st_stream(a.rgb_mask + i0 + t, (uint8_t)lc);
+    if (a.depth_mask) st_stream(a.depth_mask + i0 + t, (uint8_t)ld);
+    if (a.fused_copy) st_stream(a.fused_copy + i0 + t, (uint8_t)out);
     lab[0] = lc;
     lab[1] = ld;
     lab[2] = out;
@@ -438,7 +448,8 @@ __device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i, uint32
 template <int MC, int MD, bool kElide>
 __global__ void __launch_bounds__(kThreads, RGBDSEG_FUSED_MIN_BLOCKS(kElide))
     k_fused_ldg(const __grid_constant__ FusedArgs a) {
-    const size_t i = (size_t)blockIdx.x * kThreads + threadIdx.x;
+    const size_t i0 = (size_t)blockIdx.x * kThreads;
+    const size_t i = i0 + threadIdx.x;
     const bool active = i < a.n;
     if (!kElide && a.ahead && (threadIdx.x & 31) == 0) {
         // One bulk L2 prefetch per bank of the warp that starts about one
@@ -456,7 +467,7 @@ __global__ void __launch_bounds__(kThreads, RGBDSEG_FUSED_MIN_BLOCKS(kElide))
         }
     }
     uint32_t lab[3] = {0u, 0u, 0u};
-    if (active) fused_pixel<MC, MD, kElide>(a, i, lab);
+    if (active) fused_pixel<MC, MD, kElide>(a, i0, threadIdx.x, lab);
     if (a.gt) {  // evaluation epilogue: the masks never leave registers
         const uint32_t g = active ? (uint32_t)ld_stream(a.gt + i) : 0u;
         eval_accumulate<3>(active, a.base + i, a.stream_px, lab, g, a.counts);
@@ -870,6 +881,7 @@ cudaError_t fused_mc(const FusedArgs& a, int variant, cudaStream_t s) {
 }  // namespace
 
 cudaError_t launch_fused(const FusedArgs& a, int variant, cudaStream_t s) {
+    if (a.base % kBlockPx) return cudaErrorInvalidValue;  // tiles must be warp-aligned
     switch (a.color.M) {
         case 3: return fused_mc<3>(a, variant, s);
         case 4: return fused_mc<4>(a, variant, s);
