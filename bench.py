@@ -352,11 +352,12 @@ def main():
 
     # ---- roofline of the fused kernel ----------------------------------------
     # Dense write-back moves exactly the algorithmic 331 B/px of SURVEY 8(d)
-    # (ncu: 336.6 B/px incl. the tiled flag sectors).  The default kernel
-    # elides rewrites of unchanged state words, so its bytes are data
-    # dependent: achieved/frac use its ncu-measured DRAM bytes per pixel for
-    # this workload (profiles/traffic.json, the same 20 timed launches), and
-    # the dense-equivalent rate is reported beside it, labelled as such.
+    # (ncu: 337 B/px incl. the tiled flag sectors).  The default kernel reads
+    # only touched mixture components and writes only changed words, so its
+    # bytes are data dependent: achieved/frac use its ncu-measured DRAM bytes
+    # per pixel for this workload (profiles/traffic.json: the same 20 timed
+    # launches of the default window), and the dense-equivalent rate is
+    # reported beside it, labelled as such.
     peak, peak_src = load_peak()
     bpp = bytes_per_px(M, M)
     launch_ms = float(np.mean(kernel_ms))  # one fused launch per step on this rank
@@ -373,7 +374,11 @@ def main():
     else:
         achieved = traffic_px * npx / (launch_ms / 1e3) / 1e9
         basis = (f"ncu DRAM bytes of this kernel variant ({traffic_px} B/px, "
-                 "profiles/traffic.json): write elision skips unchanged state words")
+                 f"profiles/traffic.json, frames {START_FRAME + 5}..{START_FRAME + 24} after "
+                 f"pre-roll 0..{START_FRAME - 1}): untouched components are not read, "
+                 "unchanged words not written")
+        if start != START_FRAME or args.preroll != start:
+            basis += " [measured for the default window; this run's window differs]"
     traffic = traffic_px * npx if traffic_px is not None else None
 
     # ---- e2e: public API, pinned host frames in, fused masks out --------------
