@@ -15,6 +15,7 @@
 // HBM so every plane access of a warp is one fully coalesced 128-byte line.
 // Built with -fmad=false -prec-div=true -prec-sqrt=true -ftz=false and the
 // arithmetic spelled with explicit _rn intrinsics (gmm_pixel.cuh).
+#include <algorithm>
 #include <atomic>
 #include <cstdlib>
 #include <cstdio>
@@ -180,11 +181,12 @@ __device__ __forceinline__ uint32_t bank_pixel(Mixture<M, C>& m, const float* sr
 // components returns the full step's label and state.  The elided variant
 // reads only `need`; the dense one (N == M, need = all) rewrites everything.
 // Exact replay of a pixel the fast step refused: the whole mixture from
-// memory through the generic gmm_step.  Rare, so one out-of-line copy per
-// bank shape instead of one inlined per specialisation (code size).
+// memory (nothing was stored) through the generic gmm_step.  K1 runs it once
+// per bank after both fast steps, so there is one inlined copy per bank
+// shape instead of one per N specialisation, and no call boundary.
 template <int M, int C, bool kElide>
-__device__ __noinline__ uint32_t replay_pixel(float* s, const float (&v)[C], const MixCfg& k,
-                                              const BankView& bk, uint32_t& f) {
+__device__ __forceinline__ uint32_t replay_pixel(float* s, const float (&v)[C], const MixCfg& k,
+                                                 const BankView& bk, uint32_t& f) {
     Mixture<M, C> mm;
     load_mix<M>(s, mm);
     float wo[M];
@@ -204,7 +206,7 @@ template <int M, int C, int N, int P, bool kElide>
 __device__ __forceinline__ uint32_t step_pixel_n(float* s, const Mixture<(P > 0 ? P : 1), C>& pre,
                                                  uint32_t need, const float (&v)[C],
                                                  const MixCfg& k, const BankView& bk,
-                                                 uint32_t& f) {
+                                                 uint32_t& f, bool& replay) {
     Mixture<N, C> m;
     load_mix_need<M>(s, m, need & ~((1u << P) - 1u), bk.vvar);
 #pragma unroll
@@ -219,7 +221,7 @@ __device__ __forceinline__ uint32_t step_pixel_n(float* s, const Mixture<(P > 0 
     for (int q = 0; q < N; ++q) w_old[q] = m.w[q];
     int t = 0;
     bool ok = k.fast != 0;
-    uint32_t label = gmm_step_fast(m, v, k, t, ok);
+    const uint32_t label = gmm_step_fast(m, v, k, t, ok);
     if (ok) {
         if (kElide)
             store_mix_elide<M>(s, m, t, w_old);
@@ -227,7 +229,7 @@ __device__ __forceinline__ uint32_t step_pixel_n(float* s, const Mixture<(P > 0 
             store_mix<M>(s, m);
         f = flag_after<M>(f, t, m.w, bk);
     } else {
-        label = replay_pixel<M, C, kElide>(s, v, k, bk, f);
+        replay = true;  // nothing stored: the caller replays from memory
     }
     return label;
 }
@@ -240,7 +242,7 @@ template <int M, int C, int P, bool kElide>
 __device__ __forceinline__ uint32_t k1_bank_pixel(float* s, const Mixture<(P > 0 ? P : 1), C>& pre,
                                                   uint32_t need, int Kw, const float (&v)[C],
                                                   const MixCfg& k, const BankView& bk,
-                                                  uint32_t& f) {
+                                                  uint32_t& f, bool& replay) {
     if (!(f & 0xffu)) {
         Mixture<M, C> m;
         gmm_init(m, v, k);
@@ -249,12 +251,12 @@ __device__ __forceinline__ uint32_t k1_bank_pixel(float* s, const Mixture<(P > 0
         return 0u;
     }
     const int N = kElide ? min(Kw + 1, M) : M;
-    if (N <= 2) return step_pixel_n<M, C, 2, P, kElide>(s, pre, need, v, k, bk, f);
+    if (N <= 2) return step_pixel_n<M, C, 2, P, kElide>(s, pre, need, v, k, bk, f, replay);
     if constexpr (M >= 4)
-        if (N == 3) return step_pixel_n<M, C, 3, P, kElide>(s, pre, need, v, k, bk, f);
+        if (N == 3) return step_pixel_n<M, C, 3, P, kElide>(s, pre, need, v, k, bk, f, replay);
     if constexpr (M >= 5)
-        if (N == 4) return step_pixel_n<M, C, 4, P, kElide>(s, pre, need, v, k, bk, f);
-    return step_pixel_n<M, C, M, P, kElide>(s, pre, need, v, k, bk, f);
+        if (N == 4) return step_pixel_n<M, C, 4, P, kElide>(s, pre, need, v, k, bk, f, replay);
+    return step_pixel_n<M, C, M, P, kElide>(s, pre, need, v, k, bk, f, replay);
 }
 
 // ---------------------------------------------------------------- evaluation
@@ -338,104 +340,98 @@ __global__ void __launch_bounds__(kThreads)
 // Resident blocks per SM: the dense variant is HBM-bound at 3 (80 regs);
 // the elided one is latency-bound and gains from 4 (64 regs, 32 warps/SM)
 // despite a few spilled words (profiles/variants_r01.json).
-// Depth mixture prefetched into L1 during the colour step (see fused_pixel).
-#ifndef RGBDSEG_PREFETCH_DEPTH
-#define RGBDSEG_PREFETCH_DEPTH 1
-#endif
-#ifndef RGBDSEG_PRE_COLOR  // colour components loaded with the flag words
+#ifndef RGBDSEG_PRE_COLOR  // colour components loaded with the flag words (2 or 3)
 #define RGBDSEG_PRE_COLOR 2
 #endif
 #ifndef RGBDSEG_FUSED_MIN_BLOCKS
 #define RGBDSEG_FUSED_MIN_BLOCKS(elide) ((elide) ? 6 : 3)
 #endif
-// One pixel of K1 (thread t of the block whose first pixel is i0); returns
-// the three labels for the evaluation epilogue.  Addresses are a per-block
-// uniform base plus a 32-bit per-thread offset: tiles are warp-aligned
-// (launch_fused requires base % 32 == 0), so warp w of the block owns tile
-// (base + i0) / 32 + w.
-template <int MC, int MD, bool kElide>
-__device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i0, unsigned t,
-                                            uint32_t (&lab)[3]) {
-    constexpr unsigned SC = bank_stride(MC, 3), SD = bank_stride(MD, 1);
-    const size_t tile0 = (a.base + i0) / kBlockPx;
-    const unsigned w = t / kBlockPx, lane = t % kBlockPx;
-    float* cs = a.color.state + tile0 * SC + (w * SC + lane);
-    float* ds = a.depth.state + tile0 * SD + (w * SD + lane);
-    uint16_t* cfl = reinterpret_cast<uint16_t*>(a.color.state + tile0 * SC + bank_planes(MC, 3) * kBlockPx) +
-                    (w * SC * 2 + lane);
-    uint16_t* dfl = reinterpret_cast<uint16_t*>(a.depth.state + tile0 * SD + bank_planes(MD, 1) * kBlockPx) +
-                    (w * SD * 2 + lane);
+// First-round values of one K1 pixel: everything that does not depend on
+// its flag words -- inputs, both flag words, fusion state, colour components
+// 0..kPre-1 and depth component 0 (component 0 is touched in every
+// initialised pixel, colour component 1 in most; a loaded untouched
+// component equals its substitute).  Only the rest waits for the flags.
+constexpr int kPre = RGBDSEG_PRE_COLOR;
+struct Round1 {
+    float vc[3];
+    uint32_t raw, cf, df, out0;
+    int cpt0;
+    Mixture<kPre, 3> cpre;
+    Mixture<1, 1> dpre;
+};
 
-    // Issue every load that does not depend on the flags first: inputs,
-    // flags, fusion state, the first colour components.
-    const float vc[3] = {(float)ld_stream(a.r + i0 + t), (float)ld_stream(a.g + i0 + t),
-                         (float)ld_stream(a.b + i0 + t)};
-    const uint32_t raw = ld_stream(a.d + i0 + t);
-    const uint32_t cf = ld_stream(cfl);
-    const uint32_t df = ld_stream(dfl);
-    const uint32_t out0 = a.fuse ? ld_stream(a.out + i0 + t) : 0u;
-    const int cpt0 = a.fuse ? (int)ld_stream(a.cpt + i0 + t) : 0;
-    // First round, independent of the flags: colour components 0..kPreC-1
-    // (component 0 is touched in every initialised pixel and component 1 in
-    // most; a loaded untouched component equals its substitute) and, into
-    // L1, depth component 0.  Only the rest waits for the flag words.
-    constexpr int kPreC = MC > RGBDSEG_PRE_COLOR ? RGBDSEG_PRE_COLOR : MC;
-    Mixture<kPreC, 3> cpre;
-    load_mix<MC>(cs, cpre);
-#if RGBDSEG_PREFETCH_DEPTH
-    asm volatile("prefetch.global.L1 [%0];" ::"l"(ds));
-    asm volatile("prefetch.global.L1 [%0];" ::"l"(ds + MD * kBlockPx));
-    asm volatile("prefetch.global.L1 [%0];" ::"l"(ds + 2 * MD * kBlockPx));
-#endif
+// Per-thread addresses of K1 pixel t of the block whose first pixel is i0.
+// A per-block uniform base plus a 32-bit per-thread offset: tiles are
+// warp-aligned (launch_fused requires base % 32 == 0), so warp w of the
+// block owns tile (base + i0) / 32 + w.
+template <int MC, int MD>
+struct PixAddr {
+    float* cs;
+    float* ds;
+    uint16_t* cfl;
+    uint16_t* dfl;
+    __device__ __forceinline__ PixAddr(const FusedArgs& a, size_t i0, unsigned t) {
+        constexpr unsigned SC = bank_stride(MC, 3), SD = bank_stride(MD, 1);
+        const size_t tile0 = (a.base + i0) / kBlockPx;
+        const unsigned w = t / kBlockPx, lane = t % kBlockPx;
+        cs = a.color.state + tile0 * SC + (w * SC + lane);
+        ds = a.depth.state + tile0 * SD + (w * SD + lane);
+        cfl = reinterpret_cast<uint16_t*>(a.color.state + tile0 * SC + bank_planes(MC, 3) * kBlockPx) +
+              (w * SC * 2 + lane);
+        dfl = reinterpret_cast<uint16_t*>(a.depth.state + tile0 * SD + bank_planes(MD, 1) * kBlockPx) +
+              (w * SD * 2 + lane);
+    }
+};
+
+// K1 after the first load round: the touched-prefix dispatch, the depth
+// step, the colour step, List 1 and the stores.  Returns the three labels
+// for the evaluation epilogue.
+template <int MC, int MD, bool kElide>
+__device__ __forceinline__ void fused_core(const FusedArgs& a, size_t i0, unsigned t,
+                                           const PixAddr<MC, MD>& p, const Round1& r,
+                                           uint32_t (&lab)[3]) {
     // Components to read: the elided variant skips untouched ones and runs
     // the step on the warp's touched prefix (+1); the dense one reads all.
-    const uint32_t cneed = kElide ? ~flag_untouched<MC>(cf) : ~0u;
-    const uint32_t dneed = kElide ? ~flag_untouched<MD>(df) : ~0u;
-    const bool dstep = raw != 0 && (df & 0xffu);
+    const uint32_t cneed = kElide ? ~flag_untouched<MC>(r.cf) : ~0u;
+    const uint32_t dneed = kElide ? ~flag_untouched<MD>(r.df) : ~0u;
     int kc = MC, kd = MD;
     if (kElide) {
         const unsigned am = __activemask();
-        kc = __reduce_max_sync(am, (cf & 0xffu) ? touched_prefix<MC>(cf) : 1);
-        kd = __reduce_max_sync(am, dstep ? touched_prefix<MD>(df) : 1);
+        kc = __reduce_max_sync(am, (r.cf & 0xffu) ? touched_prefix<MC>(r.cf) : 1);
+        kd = __reduce_max_sync(am, (r.raw != 0 && (r.df & 0xffu)) ? touched_prefix<MD>(r.df) : 1);
     }
-#if RGBDSEG_PREFETCH_DEPTH
-    // The rest of the depth mixture goes to L1 now (no registers held) and
-    // into registers only after the colour step.  Only warps with a touched
-    // depth component 1 have any.
-    if (kd >= 2 && dstep) {
-        const int nd = min(kd + 1, MD);
-#pragma unroll
-        for (int q = 1; q < MD; ++q)
-            if (q < nd && ((dneed >> q) & 1u)) {
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(ds + q * kBlockPx));
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(ds + (MD + q) * kBlockPx));
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(ds + (2 * MD + q) * kBlockPx));
-            }
-    }
-#endif
 
-    // ---- colour stream (segment_color) ----
-    uint32_t cf1 = cf;
-    const uint32_t lc = k1_bank_pixel<MC, 3, kPreC, kElide>(cs, cpre, cneed, kc, vc, a.ck, a.color, cf1);
-    if (cf1 != cf) st_stream(cfl, (uint16_t)cf1);
-
+    // The two banks are independent (only List 1 needs both labels): the
+    // small depth step runs first, while the colour components wait in
+    // registers.
     // ---- depth stream (segment_depth): raw 0 = no return ----
     uint32_t ld = 0;
-    if (raw != 0) {
-        const float vd[1] = {(float)raw};
-        uint32_t df1 = df;
-        const Mixture<1, 1> none{};
-        ld = k1_bank_pixel<MD, 1, 0, kElide>(ds, none, dneed, kd, vd, a.dk, a.depth, df1);
-        if (df1 != df) st_stream(dfl, (uint16_t)df1);
+    if (r.raw != 0) {
+        const float vd[1] = {(float)r.raw};
+        uint32_t df1 = r.df;
+        bool replay = false;
+        ld = k1_bank_pixel<MD, 1, 1, kElide>(p.ds, r.dpre, dneed, kd, vd, a.dk, a.depth, df1,
+                                             replay);
+        if (replay) ld = replay_pixel<MD, 1, kElide>(p.ds, vd, a.dk, a.depth, df1);
+        if (df1 != r.df) st_stream(p.dfl, (uint16_t)df1);
     }
 
+    // ---- colour stream (segment_color) ----
+    const float vc[3] = {r.vc[0], r.vc[1], r.vc[2]};
+    uint32_t cf1 = r.cf;
+    bool replay = false;
+    uint32_t lc =
+        k1_bank_pixel<MC, 3, kPre, kElide>(p.cs, r.cpre, cneed, kc, vc, a.ck, a.color, cf1, replay);
+    if (replay) lc = replay_pixel<MC, 3, kElide>(p.cs, vc, a.ck, a.color, cf1);
+    if (cf1 != r.cf) st_stream(p.cfl, (uint16_t)cf1);
+
     // ---- List-1 fusion on the registered depth mask ----
-    uint32_t out = out0;
-    int cpt = cpt0;
+    uint32_t out = r.out0;
+    int cpt = r.cpt0;
     if (a.fuse) {
         fuse_pixel(lc, ld, a.limit, out, cpt);
-        if (!kElide || out != out0) st_stream(a.out + i0 + t, (uint8_t)out);
-        if (!kElide || cpt != cpt0) st_stream(a.cpt + i0 + t, (int8_t)cpt);
+        if (!kElide || out != r.out0) st_stream(a.out + i0 + t, (uint8_t)out);
+        if (!kElide || cpt != r.cpt0) st_stream(a.cpt + i0 + t, (int8_t)cpt);
     }
     if (a.rgb_mask) st_stream(a.rgb_mask + i0 + t, (uint8_t)lc);
     if (a.depth_mask) st_stream(a.depth_mask + i0 + t, (uint8_t)ld);
@@ -443,6 +439,25 @@ __device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i0, unsig
     lab[0] = lc;
     lab[1] = ld;
     lab[2] = out;
+}
+
+// One pixel of K1 with its first round loaded straight from global memory.
+template <int MC, int MD, bool kElide>
+__device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i0, unsigned t,
+                                            uint32_t (&lab)[3]) {
+    const PixAddr<MC, MD> p(a, i0, t);
+    Round1 r;
+    r.vc[0] = (float)ld_stream(a.r + i0 + t);
+    r.vc[1] = (float)ld_stream(a.g + i0 + t);
+    r.vc[2] = (float)ld_stream(a.b + i0 + t);
+    r.raw = ld_stream(a.d + i0 + t);
+    r.cf = ld_stream(p.cfl);
+    r.df = ld_stream(p.dfl);
+    r.out0 = a.fuse ? ld_stream(a.out + i0 + t) : 0u;
+    r.cpt0 = a.fuse ? (int)ld_stream(a.cpt + i0 + t) : 0;
+    load_mix<MC>(p.cs, r.cpre);
+    load_mix<MD>(p.ds, r.dpre);
+    fused_core<MC, MD, kElide>(a, i0, t, p, r, lab);
 }
 
 template <int MC, int MD, bool kElide>

@@ -623,7 +623,8 @@ def test_confusion_counts_kernel(R):
 
 
 @pytest.mark.parametrize("registered", [True, False])
-def test_processor_eval_epilogue_counts(R, cuda, registered):
+@pytest.mark.parametrize("variant", ["auto", "ldg"])
+def test_processor_eval_epilogue_counts(R, cuda, registered, variant):
     """The fused epilogue's per-stream counts equal counts of the returned
     masks (device frames, odd stream size, host gt on odd frames)."""
     import torch
@@ -634,7 +635,7 @@ def test_processor_eval_epilogue_counts(R, cuda, registered):
     if not registered:
         kw = dict(rig=_rig_from_array(R, random_rig(np.random.default_rng(1), w, h)),
                   registered=False)
-    proc = R.SequenceProcessor(w, h, R.RunConfig.defaults(), streams=S, **kw)
+    proc = R.SequenceProcessor(w, h, R.RunConfig.defaults(), streams=S, variant=variant, **kw)
     for f in range(12):
         fr = R.render_scenario("A", w, h, 95 + f, streams=S, seed0=2, with_gt=True)
         gt = fr["gt"] if f % 2 == 0 else to_np(fr["gt"])
