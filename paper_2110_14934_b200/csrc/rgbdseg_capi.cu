@@ -78,7 +78,17 @@ MixCfg to_k(const rgbdseg_mixture_cfg& c) {
     // gmm_step_fast divides by max(w, alpha): alpha must sit in its exact range
     const int fast = c.learning_rate >= 0x1p-60f && c.learning_rate < 0x1p61f;
     return MixCfg{c.learning_rate,  c.match_lambda,   c.background_threshold,
-                  c.initial_sigma, c.initial_weight, c.variance_floor, fast};
+                  c.initial_sigma, c.initial_weight, c.variance_floor, fast, 0.0f, 0.0f};
+}
+
+// to_k plus the untouched-component constants of a bank (gmm_step_fast's
+// kVirt): sigma = RN(sqrt(vvar)) (sqrtf is correctly rounded, like the
+// device's exact sequence) and band = RN(lambda * sigma).
+MixCfg to_k(const rgbdseg_mixture_cfg& c, float vvar) {
+    MixCfg k = to_k(c);
+    k.vsd = std::sqrt(vvar);
+    k.vband = c.match_lambda * k.vsd;
+    return k;
 }
 
 // Pointer classification with a small direct-mapped cache: a host address
@@ -787,8 +797,8 @@ static FusedArgs base_args(const rgbdseg_processor* p) {
     FusedArgs a{};
     a.color = p->color->view(p->cfg.color);
     a.depth = p->depth->view(p->cfg.depth);
-    a.ck = to_k(p->cfg.color);
-    a.dk = to_k(p->cfg.depth);
+    a.ck = to_k(p->cfg.color, p->color->vvar);
+    a.dk = to_k(p->cfg.depth, p->depth->vvar);
     a.limit = p->cfg.fusion_counter_limit;
     a.fuse = 1;
     return a;

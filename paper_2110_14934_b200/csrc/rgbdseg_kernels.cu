@@ -202,7 +202,7 @@ __device__ __forceinline__ uint32_t replay_pixel(float* s, const float (&v)[C], 
     return label;
 }
 
-template <int M, int C, int N, int P, bool kElide>
+template <int M, int C, int N, int P, bool kElide, bool kVirt>
 __device__ __forceinline__ uint32_t step_pixel_n(float* s, const Mixture<(P > 0 ? P : 1), C>& pre,
                                                  uint32_t need, const float (&v)[C],
                                                  const MixCfg& k, const BankView& bk,
@@ -221,7 +221,7 @@ __device__ __forceinline__ uint32_t step_pixel_n(float* s, const Mixture<(P > 0 
     for (int q = 0; q < N; ++q) w_old[q] = m.w[q];
     int t = 0;
     bool ok = k.fast != 0;
-    const uint32_t label = gmm_step_fast(m, v, k, t, ok);
+    const uint32_t label = gmm_step_fast<N, C, kVirt>(m, v, k, t, ok);
     if (ok) {
         if (kElide)
             store_mix_elide<M>(s, m, t, w_old);
@@ -250,13 +250,16 @@ __device__ __forceinline__ uint32_t k1_bank_pixel(float* s, const Mixture<(P > 0
         f = flag_after<M>(f, -1, m.w, bk);
         return 0u;
     }
-    const int N = kElide ? min(Kw + 1, M) : M;
-    if (N <= 2) return step_pixel_n<M, C, 2, P, kElide>(s, pre, need, v, k, bk, f, replay);
+    // Component N-1 is untouched in every lane whenever Kw < M (kVirt).
+    if (!kElide) return step_pixel_n<M, C, M, P, false, false>(s, pre, need, v, k, bk, f, replay);
+    const int N = min(Kw + 1, M);
+    if (N <= 2) return step_pixel_n<M, C, 2, P, true, true>(s, pre, need, v, k, bk, f, replay);
     if constexpr (M >= 4)
-        if (N == 3) return step_pixel_n<M, C, 3, P, kElide>(s, pre, need, v, k, bk, f, replay);
+        if (N == 3) return step_pixel_n<M, C, 3, P, true, true>(s, pre, need, v, k, bk, f, replay);
     if constexpr (M >= 5)
-        if (N == 4) return step_pixel_n<M, C, 4, P, kElide>(s, pre, need, v, k, bk, f, replay);
-    return step_pixel_n<M, C, M, P, kElide>(s, pre, need, v, k, bk, f, replay);
+        if (N == 4) return step_pixel_n<M, C, 4, P, true, true>(s, pre, need, v, k, bk, f, replay);
+    if (Kw == M - 1) return step_pixel_n<M, C, M, P, true, true>(s, pre, need, v, k, bk, f, replay);
+    return step_pixel_n<M, C, M, P, true, false>(s, pre, need, v, k, bk, f, replay);
 }
 
 // ---------------------------------------------------------------- evaluation
