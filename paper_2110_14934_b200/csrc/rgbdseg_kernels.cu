@@ -208,7 +208,10 @@ __device__ __forceinline__ uint32_t step_pixel_n(float* s, const Mixture<(P > 0 
                                                  const MixCfg& k, const BankView& bk,
                                                  uint32_t& f, bool& replay) {
     Mixture<N, C> m;
-    load_mix_need<M>(s, m, need & ~((1u << P) - 1u), bk.vvar);
+    // components P.. that are touched; with kVirt, N-1 is untouched in every
+    // lane (a compile-time zero bit: no load, constant values)
+    constexpr uint32_t kLoad = ~((1u << P) - 1u) & (kVirt ? ~(1u << (N - 1)) : ~0u);
+    load_mix_need<M>(s, m, need & kLoad, bk.vvar);
 #pragma unroll
     for (int i = 0; i < (P < N ? P : N); ++i) {  // loaded with the flags (exact values)
 #pragma unroll
