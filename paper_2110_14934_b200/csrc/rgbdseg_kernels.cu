@@ -27,7 +27,10 @@ namespace rgbdseg_b200 {
 namespace {
 std::atomic<uint64_t> g_launches{0};
 
-constexpr int kThreads = 256;
+#ifndef RGBDSEG_THREADS  // 128 measured best for K1 (64..512 tried, variants_r01.json)
+#define RGBDSEG_THREADS 128
+#endif
+constexpr int kThreads = RGBDSEG_THREADS;
 
 inline unsigned blocks_for(size_t n) {
     return static_cast<unsigned>((n + kThreads - 1) / kThreads);
@@ -268,7 +271,7 @@ __device__ __forceinline__ uint32_t k1_bank_pixel(float* s, const Mixture<(P > 0
 // ---------------------------------------------------------------- evaluation
 // Per-stream confusion counts of up to 3 methods in one block: each warp
 // popcounts ballots, warps add into shared slots for the (at most two)
-// streams a 256-pixel block can touch when streams hold >= 256 pixels, and
+// streams a block (kThreads pixels) can touch when streams hold >= kThreads pixels, and
 // one thread per nonzero counter adds it to the global int64 counters; a
 // warp whose pixels fall in another stream adds directly.  tn is derived
 // from the counted pixels: eval.cpp:17-28 assigns every pixel exactly one.
@@ -343,14 +346,14 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // ---------------------------------------------------------------- K1 fused
-// Resident blocks per SM: the dense variant is HBM-bound at 3 (80 regs);
-// the elided one is latency-bound and gains from 4 (64 regs, 32 warps/SM)
-// despite a few spilled words (profiles/variants_r01.json).
+// Resident 128-thread blocks per SM: the dense variant is HBM-bound at 6
+// (80 regs, 24 warps/SM); the elided one is issue/latency-bound and gains
+// from 12 (40 regs, 48 warps/SM) despite spills (profiles/variants_r01.json).
 #ifndef RGBDSEG_PRE_COLOR  // colour components loaded with the flag words (2 or 3)
 #define RGBDSEG_PRE_COLOR 2
 #endif
 #ifndef RGBDSEG_FUSED_MIN_BLOCKS
-#define RGBDSEG_FUSED_MIN_BLOCKS(elide) ((elide) ? 6 : 3)
+#define RGBDSEG_FUSED_MIN_BLOCKS(elide) ((elide) ? 12 : 6)
 #endif
 // First-round values of one K1 pixel: everything that does not depend on
 // its flag words -- inputs, both flag words, fusion state, colour components
