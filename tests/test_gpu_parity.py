@@ -977,3 +977,98 @@ def test_mask_needs_the_creation_sigma(R, port):
                 assert (flag_words(R, bank) >> 8 == expect).all()
         assert bank.planes().tobytes() == ob.planes().tobytes()
         check_untouched_invariant(bank, flag_words(R, bank), oc.initial_sigma)
+
+
+def set_flag_words(R, bank, words):
+    """Write raw uint16 flag words (pixel order) into a bank's tiles."""
+    import ctypes as C
+
+    import torch
+
+    t, bb, nb = C.c_void_p(), C.c_size_t(), C.c_size_t()
+    R._lib.lib.rgbdseg_bank_device_ptrs(bank._h, C.byref(t), C.byref(bb), C.byref(nb))
+    per = bb.value // 2
+
+    class Raw:
+        __cuda_array_interface__ = {"shape": (nb.value * per,), "typestr": "<i2",
+                                    "data": (t.value, False), "version": 3}
+
+    torch.cuda.synchronize()
+    raw = torch.as_tensor(Raw(), device="cuda").view(nb.value, per)
+    npl = R._lib.lib.rgbdseg_bank_planes(bank._h)
+    pad = np.zeros(nb.value * 32, np.uint16)
+    pad[: bank.npx] = words
+    raw[:, npl * 64: npl * 64 + 32] = torch.from_numpy(pad.view(np.int16).reshape(nb.value, 32)).cuda()
+    torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("variant", ["auto", "ldg"])
+def test_fused_random_untouched_masks_vs_oracle(R, port, variant):
+    """Arbitrary untouched masks -- suffixes of every length, non-suffix
+    sets (the full-width path), touched components with weight +0 (fitness
+    ties with the untouched ones) -- written straight into the flag words
+    over states that honour them: K1 equals the oracle, masks and every bank
+    word, frame after frame."""
+    rng = np.random.default_rng(23)
+    S, w, h, M = 2, 64, 40, 5
+    n = w * h
+    oc, od = O.color_cfg(M), O.depth_cfg(M)
+    cfg = R.RunConfig.defaults()
+    cfg.color_gmm, cfg.depth_gmm = rcfg(R, oc), rcfg(R, od)
+    proc = R.SequenceProcessor(w, h, cfg, streams=S, variant=variant)
+    ops = [O.PortProcessor(port, n, oc, od) for _ in range(S)]
+    sc = [O.PortScene(port, "A", w, h, seed=7 + s) for s in range(S)]
+    frames = [[x.render(f) for x in sc] for f in range(40, 52)]
+
+    def state(Ch, sigma, lo, hi):
+        P = np.zeros((M * Ch + 2 * M, S * n), np.float32)
+        # per warp (32 pixels): 0 = short suffixes (K 1..2) with non-suffix
+        # lanes mixed in (their first untouched index is low, a later one is
+        # touched); 1 = suffixes of any length; 2 = random sets / none
+        mode = np.repeat(rng.integers(0, 3, (S * n + 31) // 32), 32)[: S * n]
+        U = np.zeros((S * n, M), bool)
+        short = rng.integers(1, 3, S * n)
+        anyk = rng.integers(1, M + 1, S * n)
+        odd = rng.random(S * n) < 0.3
+        rnd = rng.random((S * n, M)) < 0.5
+        for i in range(1, M):
+            U[:, i] = np.where(mode == 0, (i >= short) & ~(odd & (i == M - 2)),
+                               np.where(mode == 1, i >= anyk, rnd[:, i]))
+        for i in range(M):
+            P[i * Ch:(i + 1) * Ch] = rng.uniform(lo, hi, (Ch, S * n))
+            P[M * Ch + i] = rng.choice(np.array([9.0, 40.0, 300.0, 2500.0], np.float32), S * n)
+            wt = rng.uniform(0.02, 1.0, S * n).astype(np.float32)
+            wt[rng.random(S * n) < 0.1] = 0.0  # touched but weight +0
+            P[M * Ch + M + i] = wt
+            u = U[:, i]
+            P[i * Ch:(i + 1) * Ch, u] = 0.0
+            P[M * Ch + i, u] = np.float32(sigma) * np.float32(sigma)
+            P[M * Ch + M + i, u] = 0.0
+        words = (1 | (U[:, 1:] * (1 << np.arange(9, 9 + M - 1))).sum(1)).astype(np.uint16)
+        return P, words
+
+    for bank, ob_of, Ch, c, lo, hi in ((proc.color_bank(), lambda o: o.color, 3, oc, 0, 255),
+                                        (proc.depth_bank(), lambda o: o.depth, 1, od, 500, 5000)):
+        P, words = state(Ch, c.initial_sigma, lo, hi)
+        for p in range(P.shape[0]):
+            bank.upload_plane(p, P[p].reshape(S, h, w))
+        set_flag_words(R, bank, words)
+        assert np.array_equal(flag_words(R, bank), words)
+        for s in range(S):
+            ob = ob_of(ops[s])
+            ob.planes()[:] = P[:, s * n:(s + 1) * n]
+            ob.flags[:] = 1
+    for f, frs in enumerate(frames):
+        st = lambda k: np.stack([getattr(fr, k) for fr in frs])
+        m = proc.process(st("r"), st("g"), st("b"), st("depth"))
+        for s in range(S):
+            rgb, dep, fused = ops[s].process(frs[s].r, frs[s].g, frs[s].b, frs[s].depth)
+            assert np.array_equal(m.rgb[s].ravel(), rgb), (f, s)
+            assert np.array_equal(m.depth[s].ravel(), dep), (f, s)
+            assert np.array_equal(m.fused[s].ravel(), fused), (f, s)
+        for bank, ob_of in ((proc.color_bank(), lambda o: o.color), (proc.depth_bank(), lambda o: o.depth)):
+            got = bank.planes()
+            for s in range(S):
+                assert got[:, s * n:(s + 1) * n].tobytes() == ob_of(ops[s]).planes().tobytes(), (f, s)
+    check_untouched_invariant(proc.color_bank(), flag_words(R, proc.color_bank()), oc.initial_sigma)
+    check_untouched_invariant(proc.depth_bank(), flag_words(R, proc.depth_bank()), od.initial_sigma)
