@@ -481,7 +481,7 @@ def main():
                          "kernel_ms_min_max": [round(min(kernel_ms), 4), round(max(kernel_ms), 4)],
                          "dense_algorithmic_bytes_per_px": bpp,
                          "dense_equivalent_gbs": round(dense_gbs, 1),
-                         "dense_equivalent_frac": round(dense_gbs / peak, 4)},
+                         "x_dense_roofline_ceiling": round(dense_gbs / peak, 4)},
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_value, 2), "unit": "Mpix/s",
                     "h2d_bytes_per_step": 5 * npx, "d2h_bytes_per_step": npx,

@@ -1072,3 +1072,35 @@ def test_fused_random_untouched_masks_vs_oracle(R, port, variant):
                 assert got[:, s * n:(s + 1) * n].tobytes() == ob_of(ops[s]).planes().tobytes(), (f, s)
     check_untouched_invariant(proc.color_bank(), flag_words(R, proc.color_bank()), oc.initial_sigma)
     check_untouched_invariant(proc.depth_bank(), flag_words(R, proc.depth_bank()), od.initial_sigma)
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="compiled reference (oracle/_ref) absent")
+def test_config4_four_vga_streams_300_frames_vs_reference(R, cuda):
+    """SURVEY 8(d) config-4 parity at full size: 4 of the 256 VGA streams
+    (seeds 1..4), all 300 frames of scenario A with depth holes, through the
+    default K1 from host frames, against the compiled reference's
+    SequenceProcessor (all host threads): every rgb / depth / fused mask,
+    then every bank word and flag."""
+    S, w, h, M = 4, 640, 480, 5
+    n = w * h
+    cfg = R.RunConfig.defaults()
+    cfg.color_gmm.components = cfg.depth_gmm.components = M
+    proc = R.SequenceProcessor(w, h, cfg, streams=S)
+    ref = O.Ref()
+    refs = [O.RefProcessor(ref, w, h, O.color_cfg(M), O.depth_cfg(M), workers=os.cpu_count() or 1)
+            for _ in range(S)]
+    for f in range(300):
+        fr = {k: to_np(v) for k, v in R.render_scenario("A", w, h, f, streams=S, seed0=1).items()}
+        d = holes(fr["depth"], f)
+        m = proc.process(fr["r"], fr["g"], fr["b"], d)
+        for s in range(S):
+            rgb, dep, fused = refs[s].process(fr["r"][s], fr["g"][s], fr["b"][s], d[s])
+            assert np.array_equal(m.rgb[s].ravel(), rgb), (f, s)
+            assert np.array_equal(m.depth[s].ravel(), dep), (f, s)
+            assert np.array_equal(m.fused[s].ravel(), fused), (f, s)
+    for which, bank in ((0, proc.color_bank()), (1, proc.depth_bank())):
+        P = bank.planes()
+        fl = bank.initialized_plane().reshape(-1)
+        for s in range(S):
+            assert P[:, s * n:(s + 1) * n].tobytes() == refs[s].bank_planes(which).tobytes(), s
+            assert np.array_equal(fl[s * n:(s + 1) * n], refs[s].flags(which)), s
