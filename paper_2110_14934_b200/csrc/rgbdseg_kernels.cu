@@ -36,7 +36,26 @@ inline unsigned blocks_for(size_t n) {
     return static_cast<unsigned>((n + kThreads - 1) / kThreads);
 }
 
-// Streaming loads/stores: every state word is touched once per frame.
+// Loads/stores of the hot path.  H = false: streaming (evict-first) hints,
+// every word is touched once per frame -- the dense K1 and the single-bank
+// kernels.  H = true (elided K1): loads cached in L2 only (ld.global.cg), so
+// L1 holds the kernel's register spills, and default write-back stores;
+// measured 6% faster for the elided K1 and 5% slower for the dense one
+// (profiles/variants_r01.json).
+template <bool H, typename T>
+__device__ __forceinline__ T ld_h(const T* p) {
+    if constexpr (H)
+        return __ldcg(p);
+    else
+        return __ldcs(p);
+}
+template <bool H, typename T>
+__device__ __forceinline__ void st_h(T* p, T v) {
+    if constexpr (H)
+        *p = v;
+    else
+        __stcs(p, v);
+}
 template <typename T>
 __device__ __forceinline__ T ld_stream(const T* p) {
     return __ldcs(p);
@@ -93,65 +112,65 @@ __device__ __forceinline__ uint32_t flag_after(uint32_t f, int touched, const fl
 
 // Mixture I/O on a bank of layout L components: components 0..N-1 of the
 // pixel at `s` (N <= L).
-template <int L, int N, int C>
+template <int L, bool H = false, int N, int C>
 __device__ __forceinline__ void load_mix(const float* s, Mixture<N, C>& m) {
 #pragma unroll
     for (int i = 0; i < N; ++i)
 #pragma unroll
-        for (int c = 0; c < C; ++c) m.mu[i][c] = ld_stream(s + (i * C + c) * kBlockPx);
+        for (int c = 0; c < C; ++c) m.mu[i][c] = ld_h<H>(s + (i * C + c) * kBlockPx);
 #pragma unroll
-    for (int i = 0; i < N; ++i) m.var[i] = ld_stream(s + (L * C + i) * kBlockPx);
+    for (int i = 0; i < N; ++i) m.var[i] = ld_h<H>(s + (L * C + i) * kBlockPx);
 #pragma unroll
-    for (int i = 0; i < N; ++i) m.w[i] = ld_stream(s + (L * C + L + i) * kBlockPx);
+    for (int i = 0; i < N; ++i) m.w[i] = ld_h<H>(s + (L * C + L + i) * kBlockPx);
 }
 
 // load_mix for the components whose bit is set in `need`; the others are
 // untouched (flag word) and take their known values without a memory access.
-template <int L, int N, int C>
+template <int L, bool H = false, int N, int C>
 __device__ __forceinline__ void load_mix_need(const float* s, Mixture<N, C>& m, uint32_t need,
                                               float vvar) {
 #pragma unroll
     for (int i = 0; i < N; ++i) {
         const bool ld = (need >> i) & 1u;
 #pragma unroll
-        for (int c = 0; c < C; ++c) m.mu[i][c] = ld ? ld_stream(s + (i * C + c) * kBlockPx) : 0.0f;
-        m.var[i] = ld ? ld_stream(s + (L * C + i) * kBlockPx) : vvar;
-        m.w[i] = ld ? ld_stream(s + (L * C + L + i) * kBlockPx) : 0.0f;
+        for (int c = 0; c < C; ++c) m.mu[i][c] = ld ? ld_h<H>(s + (i * C + c) * kBlockPx) : 0.0f;
+        m.var[i] = ld ? ld_h<H>(s + (L * C + i) * kBlockPx) : vvar;
+        m.w[i] = ld ? ld_h<H>(s + (L * C + L + i) * kBlockPx) : 0.0f;
     }
 }
 
 // Dense store (ModelBank::scatter, segmenter.cpp:49-56).
-template <int L, int N, int C>
+template <int L, bool H = false, int N, int C>
 __device__ __forceinline__ void store_mix(float* s, const Mixture<N, C>& m) {
 #pragma unroll
     for (int i = 0; i < N; ++i)
 #pragma unroll
-        for (int c = 0; c < C; ++c) st_stream(s + (i * C + c) * kBlockPx, m.mu[i][c]);
+        for (int c = 0; c < C; ++c) st_h<H>(s + (i * C + c) * kBlockPx, m.mu[i][c]);
 #pragma unroll
-    for (int i = 0; i < N; ++i) st_stream(s + (L * C + i) * kBlockPx, m.var[i]);
+    for (int i = 0; i < N; ++i) st_h<H>(s + (L * C + i) * kBlockPx, m.var[i]);
 #pragma unroll
-    for (int i = 0; i < N; ++i) st_stream(s + (L * C + L + i) * kBlockPx, m.w[i]);
+    for (int i = 0; i < N; ++i) st_h<H>(s + (L * C + L + i) * kBlockPx, m.w[i]);
 }
 
 // Elided store: identical memory image to store_mix, but words whose bits
 // did not change are not rewritten.  Only the matched / replaced component's
 // mean and variance can change in a step (mixture.cpp:105-113, 125-128); the
 // weights are compared individually.
-template <int L, int N, int C>
+template <int L, bool H = false, int N, int C>
 __device__ __forceinline__ void store_mix_elide(float* s, const Mixture<N, C>& m, int touched,
                                                 const float (&w_old)[N]) {
 #pragma unroll
     for (int i = 0; i < N; ++i) {
         if (touched == i) {
 #pragma unroll
-            for (int c = 0; c < C; ++c) st_stream(s + (i * C + c) * kBlockPx, m.mu[i][c]);
-            st_stream(s + (L * C + i) * kBlockPx, m.var[i]);
+            for (int c = 0; c < C; ++c) st_h<H>(s + (i * C + c) * kBlockPx, m.mu[i][c]);
+            st_h<H>(s + (L * C + i) * kBlockPx, m.var[i]);
         }
     }
 #pragma unroll
     for (int i = 0; i < N; ++i)
         if (__float_as_uint(m.w[i]) != __float_as_uint(w_old[i]))
-            st_stream(s + (L * C + L + i) * kBlockPx, m.w[i]);
+            st_h<H>(s + (L * C + L + i) * kBlockPx, m.w[i]);
 }
 
 // run_bank's per-pixel body (segmenter.cpp:80-96) on a mixture loaded from
@@ -191,16 +210,16 @@ template <int M, int C, bool kElide>
 __device__ __forceinline__ uint32_t replay_pixel(float* s, const float (&v)[C], const MixCfg& k,
                                                  const BankView& bk, uint32_t& f) {
     Mixture<M, C> mm;
-    load_mix<M>(s, mm);
+    load_mix<M, kElide>(s, mm);
     float wo[M];
 #pragma unroll
     for (int q = 0; q < M; ++q) wo[q] = mm.w[q];
     int t = 0;
     const uint32_t label = gmm_step(mm, v, k, t);
     if (kElide)
-        store_mix_elide<M>(s, mm, t, wo);
+        store_mix_elide<M, kElide>(s, mm, t, wo);
     else
-        store_mix<M>(s, mm);
+        store_mix<M, kElide>(s, mm);
     f = flag_after<M>(f, t, mm.w, bk);
     return label;
 }
@@ -214,7 +233,7 @@ __device__ __forceinline__ uint32_t step_pixel_n(float* s, const Mixture<(P > 0 
     // components P.. that are touched; with kVirt, N-1 is untouched in every
     // lane (a compile-time zero bit: no load, constant values)
     constexpr uint32_t kLoad = ~((1u << P) - 1u) & (kVirt ? ~(1u << (N - 1)) : ~0u);
-    load_mix_need<M>(s, m, need & kLoad, bk.vvar);
+    load_mix_need<M, kElide>(s, m, need & kLoad, bk.vvar);
 #pragma unroll
     for (int i = 0; i < (P < N ? P : N); ++i) {  // loaded with the flags (exact values)
 #pragma unroll
@@ -230,9 +249,9 @@ __device__ __forceinline__ uint32_t step_pixel_n(float* s, const Mixture<(P > 0 
     const uint32_t label = gmm_step_fast<N, C, kVirt>(m, v, k, t, ok);
     if (ok) {
         if (kElide)
-            store_mix_elide<M>(s, m, t, w_old);
+            store_mix_elide<M, kElide>(s, m, t, w_old);
         else
-            store_mix<M>(s, m);
+            store_mix<M, kElide>(s, m);
         f = flag_after<M>(f, t, m.w, bk);
     } else {
         replay = true;  // nothing stored: the caller replays from memory
@@ -252,7 +271,7 @@ __device__ __forceinline__ uint32_t k1_bank_pixel(float* s, const Mixture<(P > 0
     if (!(f & 0xffu)) {
         Mixture<M, C> m;
         gmm_init(m, v, k);
-        store_mix<M>(s, m);
+        store_mix<M, kElide>(s, m);
         f = flag_after<M>(f, -1, m.w, bk);
         return 0u;
     }
@@ -422,7 +441,7 @@ __device__ __forceinline__ void fused_core(const FusedArgs& a, size_t i0, unsign
         ld = k1_bank_pixel<MD, 1, 1, kElide>(p.ds, r.dpre, dneed, kd, vd, a.dk, a.depth, df1,
                                              replay);
         if (replay) ld = replay_pixel<MD, 1, kElide>(p.ds, vd, a.dk, a.depth, df1);
-        if (df1 != r.df) st_stream(p.dfl, (uint16_t)df1);
+        if (df1 != r.df) st_h<kElide>(p.dfl, (uint16_t)df1);
     }
 
     // ---- colour stream (segment_color) ----
@@ -432,19 +451,19 @@ __device__ __forceinline__ void fused_core(const FusedArgs& a, size_t i0, unsign
     uint32_t lc =
         k1_bank_pixel<MC, 3, kPre, kElide>(p.cs, r.cpre, cneed, kc, vc, a.ck, a.color, cf1, replay);
     if (replay) lc = replay_pixel<MC, 3, kElide>(p.cs, vc, a.ck, a.color, cf1);
-    if (cf1 != r.cf) st_stream(p.cfl, (uint16_t)cf1);
+    if (cf1 != r.cf) st_h<kElide>(p.cfl, (uint16_t)cf1);
 
     // ---- List-1 fusion on the registered depth mask ----
     uint32_t out = r.out0;
     int cpt = r.cpt0;
     if (a.fuse) {
         fuse_pixel(lc, ld, a.limit, out, cpt);
-        if (!kElide || out != r.out0) st_stream(a.out + i0 + t, (uint8_t)out);
-        if (!kElide || cpt != r.cpt0) st_stream(a.cpt + i0 + t, (int8_t)cpt);
+        if (!kElide || out != r.out0) st_h<kElide>(a.out + i0 + t, (uint8_t)out);
+        if (!kElide || cpt != r.cpt0) st_h<kElide>(a.cpt + i0 + t, (int8_t)cpt);
     }
-    if (a.rgb_mask) st_stream(a.rgb_mask + i0 + t, (uint8_t)lc);
-    if (a.depth_mask) st_stream(a.depth_mask + i0 + t, (uint8_t)ld);
-    if (a.fused_copy) st_stream(a.fused_copy + i0 + t, (uint8_t)out);
+    if (a.rgb_mask) st_h<kElide>(a.rgb_mask + i0 + t, (uint8_t)lc);
+    if (a.depth_mask) st_h<kElide>(a.depth_mask + i0 + t, (uint8_t)ld);
+    if (a.fused_copy) st_h<kElide>(a.fused_copy + i0 + t, (uint8_t)out);
     lab[0] = lc;
     lab[1] = ld;
     lab[2] = out;
@@ -456,16 +475,16 @@ __device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i0, unsig
                                             uint32_t (&lab)[3]) {
     const PixAddr<MC, MD> p(a, i0, t);
     Round1 r;
-    r.vc[0] = (float)ld_stream(a.r + i0 + t);
-    r.vc[1] = (float)ld_stream(a.g + i0 + t);
-    r.vc[2] = (float)ld_stream(a.b + i0 + t);
-    r.raw = ld_stream(a.d + i0 + t);
-    r.cf = ld_stream(p.cfl);
-    r.df = ld_stream(p.dfl);
-    r.out0 = a.fuse ? ld_stream(a.out + i0 + t) : 0u;
-    r.cpt0 = a.fuse ? (int)ld_stream(a.cpt + i0 + t) : 0;
-    load_mix<MC>(p.cs, r.cpre);
-    load_mix<MD>(p.ds, r.dpre);
+    r.vc[0] = (float)ld_h<kElide>(a.r + i0 + t);
+    r.vc[1] = (float)ld_h<kElide>(a.g + i0 + t);
+    r.vc[2] = (float)ld_h<kElide>(a.b + i0 + t);
+    r.raw = ld_h<kElide>(a.d + i0 + t);
+    r.cf = ld_h<kElide>(p.cfl);
+    r.df = ld_h<kElide>(p.dfl);
+    r.out0 = a.fuse ? ld_h<kElide>(a.out + i0 + t) : 0u;
+    r.cpt0 = a.fuse ? (int)ld_h<kElide>(a.cpt + i0 + t) : 0;
+    load_mix<MC, kElide>(p.cs, r.cpre);
+    load_mix<MD, kElide>(p.ds, r.dpre);
     fused_core<MC, MD, kElide>(a, i0, t, p, r, lab);
 }
 
