@@ -368,6 +368,12 @@ __global__ void __launch_bounds__(kThreads)
 // Resident 128-thread blocks per SM: the dense variant is HBM-bound at 6
 // (80 regs, 24 warps/SM); the elided one is issue/latency-bound and gains
 // from 12 (40 regs, 48 warps/SM) despite spills (profiles/variants_r01.json).
+#ifndef RGBDSEG_LAZY_FLAGS  // flag-word pointers derived from the state pointers on use
+#define RGBDSEG_LAZY_FLAGS 1
+#endif
+#ifndef RGBDSEG_LATE_FUSION  // fusion state read at List 1 (prefetched to L1)
+#define RGBDSEG_LATE_FUSION 1
+#endif
 #ifndef RGBDSEG_PRE_COLOR  // colour components loaded with the flag words (2 or 3)
 #define RGBDSEG_PRE_COLOR 2
 #endif
@@ -404,11 +410,26 @@ struct PixAddr {
         const unsigned w = t / kBlockPx, lane = t % kBlockPx;
         cs = a.color.state + tile0 * SC + (w * SC + lane);
         ds = a.depth.state + tile0 * SD + (w * SD + lane);
+#if !RGBDSEG_LAZY_FLAGS
         cfl = reinterpret_cast<uint16_t*>(a.color.state + tile0 * SC + bank_planes(MC, 3) * kBlockPx) +
               (w * SC * 2 + lane);
         dfl = reinterpret_cast<uint16_t*>(a.depth.state + tile0 * SD + bank_planes(MD, 1) * kBlockPx) +
               (w * SD * 2 + lane);
+#endif
     }
+#if RGBDSEG_LAZY_FLAGS  // flag word of the pixel at cs: byte offset NP*128 - 2*lane
+    __device__ __forceinline__ uint16_t* cflag() const {
+        const unsigned lane = threadIdx.x % kBlockPx;
+        return reinterpret_cast<uint16_t*>(reinterpret_cast<char*>(cs) + bank_planes(MC, 3) * 128 - 2 * lane);
+    }
+    __device__ __forceinline__ uint16_t* dflag() const {
+        const unsigned lane = threadIdx.x % kBlockPx;
+        return reinterpret_cast<uint16_t*>(reinterpret_cast<char*>(ds) + bank_planes(MD, 1) * 128 - 2 * lane);
+    }
+#else
+    __device__ __forceinline__ uint16_t* cflag() const { return cfl; }
+    __device__ __forceinline__ uint16_t* dflag() const { return dfl; }
+#endif
 };
 
 // K1 after the first load round: the touched-prefix dispatch, the depth
@@ -441,7 +462,7 @@ __device__ __forceinline__ void fused_core(const FusedArgs& a, size_t i0, unsign
         ld = k1_bank_pixel<MD, 1, 1, kElide>(p.ds, r.dpre, dneed, kd, vd, a.dk, a.depth, df1,
                                              replay);
         if (replay) ld = replay_pixel<MD, 1, kElide>(p.ds, vd, a.dk, a.depth, df1);
-        if (df1 != r.df) st_h<kElide>(p.dfl, (uint16_t)df1);
+        if (df1 != r.df) st_h<kElide>(p.dflag(), (uint16_t)df1);
     }
 
     // ---- colour stream (segment_color) ----
@@ -451,15 +472,22 @@ __device__ __forceinline__ void fused_core(const FusedArgs& a, size_t i0, unsign
     uint32_t lc =
         k1_bank_pixel<MC, 3, kPre, kElide>(p.cs, r.cpre, cneed, kc, vc, a.ck, a.color, cf1, replay);
     if (replay) lc = replay_pixel<MC, 3, kElide>(p.cs, vc, a.ck, a.color, cf1);
-    if (cf1 != r.cf) st_h<kElide>(p.cfl, (uint16_t)cf1);
+    if (cf1 != r.cf) st_h<kElide>(p.cflag(), (uint16_t)cf1);
 
     // ---- List-1 fusion on the registered depth mask ----
-    uint32_t out = r.out0;
-    int cpt = r.cpt0;
+#if RGBDSEG_LATE_FUSION
+    const uint32_t out0 = a.fuse ? a.out[i0 + t] : 0u;
+    const int cpt0 = a.fuse ? (int)a.cpt[i0 + t] : 0;
+#else
+    const uint32_t out0 = r.out0;
+    const int cpt0 = r.cpt0;
+#endif
+    uint32_t out = out0;
+    int cpt = cpt0;
     if (a.fuse) {
         fuse_pixel(lc, ld, a.limit, out, cpt);
-        if (!kElide || out != r.out0) st_h<kElide>(a.out + i0 + t, (uint8_t)out);
-        if (!kElide || cpt != r.cpt0) st_h<kElide>(a.cpt + i0 + t, (int8_t)cpt);
+        if (!kElide || out != out0) st_h<kElide>(a.out + i0 + t, (uint8_t)out);
+        if (!kElide || cpt != cpt0) st_h<kElide>(a.cpt + i0 + t, (int8_t)cpt);
     }
     if (a.rgb_mask) st_h<kElide>(a.rgb_mask + i0 + t, (uint8_t)lc);
     if (a.depth_mask) st_h<kElide>(a.depth_mask + i0 + t, (uint8_t)ld);
@@ -479,10 +507,17 @@ __device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i0, unsig
     r.vc[1] = (float)ld_h<kElide>(a.g + i0 + t);
     r.vc[2] = (float)ld_h<kElide>(a.b + i0 + t);
     r.raw = ld_h<kElide>(a.d + i0 + t);
-    r.cf = ld_h<kElide>(p.cfl);
-    r.df = ld_h<kElide>(p.dfl);
+    r.cf = ld_h<kElide>(p.cflag());
+    r.df = ld_h<kElide>(p.dflag());
+#if RGBDSEG_LATE_FUSION
+    if (a.fuse) {  // into L1 now, read at List 1
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(a.out + i0 + t));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(a.cpt + i0 + t));
+    }
+#else
     r.out0 = a.fuse ? ld_h<kElide>(a.out + i0 + t) : 0u;
     r.cpt0 = a.fuse ? (int)ld_h<kElide>(a.cpt + i0 + t) : 0;
+#endif
     load_mix<MC, kElide>(p.cs, r.cpre);
     load_mix<MD, kElide>(p.ds, r.dpre);
     fused_core<MC, MD, kElide>(a, i0, t, p, r, lab);
