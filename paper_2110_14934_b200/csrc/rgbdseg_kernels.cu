@@ -368,6 +368,9 @@ __global__ void __launch_bounds__(kThreads)
 // Resident 128-thread blocks per SM: the dense variant is HBM-bound at 6
 // (80 regs, 24 warps/SM); the elided one is issue/latency-bound and gains
 // from 12 (40 regs, 48 warps/SM) despite spills (profiles/variants_r01.json).
+#ifndef RGBDSEG_PRE_COLOR_L1  // first colour components via an L1 prefetch, not registers
+#define RGBDSEG_PRE_COLOR_L1 0
+#endif
 #ifndef RGBDSEG_LAZY_FLAGS  // flag-word pointers derived from the state pointers on use
 #define RGBDSEG_LAZY_FLAGS 1
 #endif
@@ -467,10 +470,22 @@ __device__ __forceinline__ void fused_core(const FusedArgs& a, size_t i0, unsign
 
     // ---- colour stream (segment_color) ----
     const float vc[3] = {r.vc[0], r.vc[1], r.vc[2]};
+#if RGBDSEG_PRE_COLOR_L1
+    Mixture<kPre, 3> cpre;  // L1 hits (prefetched with the first round)
+#pragma unroll
+    for (int q = 0; q < kPre; ++q) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) cpre.mu[q][c] = p.cs[(q * 3 + c) * kBlockPx];
+        cpre.var[q] = p.cs[(MC * 3 + q) * kBlockPx];
+        cpre.w[q] = p.cs[(MC * 4 + q) * kBlockPx];
+    }
+#else
+    const Mixture<kPre, 3>& cpre = r.cpre;
+#endif
     uint32_t cf1 = r.cf;
     bool replay = false;
     uint32_t lc =
-        k1_bank_pixel<MC, 3, kPre, kElide>(p.cs, r.cpre, cneed, kc, vc, a.ck, a.color, cf1, replay);
+        k1_bank_pixel<MC, 3, kPre, kElide>(p.cs, cpre, cneed, kc, vc, a.ck, a.color, cf1, replay);
     if (replay) lc = replay_pixel<MC, 3, kElide>(p.cs, vc, a.ck, a.color, cf1);
     if (cf1 != r.cf) st_h<kElide>(p.cflag(), (uint16_t)cf1);
 
@@ -518,7 +533,19 @@ __device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i0, unsig
     r.out0 = a.fuse ? ld_h<kElide>(a.out + i0 + t) : 0u;
     r.cpt0 = a.fuse ? (int)ld_h<kElide>(a.cpt + i0 + t) : 0;
 #endif
+#if RGBDSEG_PRE_COLOR_L1
+    // colour components 0..kPre-1 into L1 now, into registers at the colour step
+#pragma unroll
+    for (int q = 0; q < kPre; ++q) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(p.cs + (q * 3 + c) * kBlockPx));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(p.cs + (MC * 3 + q) * kBlockPx));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(p.cs + (MC * 4 + q) * kBlockPx));
+    }
+#else
     load_mix<MC, kElide>(p.cs, r.cpre);
+#endif
     load_mix<MD, kElide>(p.ds, r.dpre);
     fused_core<MC, MD, kElide>(a, i0, t, p, r, lab);
 }
