@@ -368,15 +368,6 @@ __global__ void __launch_bounds__(kThreads)
 // Resident 128-thread blocks per SM: the dense variant is HBM-bound at 6
 // (80 regs, 24 warps/SM); the elided one is issue/latency-bound and gains
 // from 12 (40 regs, 48 warps/SM) despite spills (profiles/variants_r01.json).
-#ifndef RGBDSEG_PRE_COLOR_L1  // first colour components via an L1 prefetch, not registers
-#define RGBDSEG_PRE_COLOR_L1 0
-#endif
-#ifndef RGBDSEG_LAZY_FLAGS  // flag-word pointers derived from the state pointers on use
-#define RGBDSEG_LAZY_FLAGS 1
-#endif
-#ifndef RGBDSEG_LATE_FUSION  // fusion state read at List 1 (prefetched to L1)
-#define RGBDSEG_LATE_FUSION 1
-#endif
 #ifndef RGBDSEG_PRE_COLOR  // colour components loaded with the flag words (2 or 3)
 #define RGBDSEG_PRE_COLOR 2
 #endif
@@ -384,15 +375,14 @@ __global__ void __launch_bounds__(kThreads)
 #define RGBDSEG_FUSED_MIN_BLOCKS(elide) ((elide) ? 12 : 6)
 #endif
 // First-round values of one K1 pixel: everything that does not depend on
-// its flag words -- inputs, both flag words, fusion state, colour components
+// its flag words -- inputs, both flag words, colour components
 // 0..kPre-1 and depth component 0 (component 0 is touched in every
 // initialised pixel, colour component 1 in most; a loaded untouched
 // component equals its substitute).  Only the rest waits for the flags.
 constexpr int kPre = RGBDSEG_PRE_COLOR;
 struct Round1 {
     float vc[3];
-    uint32_t raw, cf, df, out0;
-    int cpt0;
+    uint32_t raw, cf, df;
     Mixture<kPre, 3> cpre;
     Mixture<1, 1> dpre;
 };
@@ -405,22 +395,16 @@ template <int MC, int MD>
 struct PixAddr {
     float* cs;
     float* ds;
-    uint16_t* cfl;
-    uint16_t* dfl;
     __device__ __forceinline__ PixAddr(const FusedArgs& a, size_t i0, unsigned t) {
         constexpr unsigned SC = bank_stride(MC, 3), SD = bank_stride(MD, 1);
         const size_t tile0 = (a.base + i0) / kBlockPx;
         const unsigned w = t / kBlockPx, lane = t % kBlockPx;
         cs = a.color.state + tile0 * SC + (w * SC + lane);
         ds = a.depth.state + tile0 * SD + (w * SD + lane);
-#if !RGBDSEG_LAZY_FLAGS
-        cfl = reinterpret_cast<uint16_t*>(a.color.state + tile0 * SC + bank_planes(MC, 3) * kBlockPx) +
-              (w * SC * 2 + lane);
-        dfl = reinterpret_cast<uint16_t*>(a.depth.state + tile0 * SD + bank_planes(MD, 1) * kBlockPx) +
-              (w * SD * 2 + lane);
-#endif
     }
-#if RGBDSEG_LAZY_FLAGS  // flag word of the pixel at cs: byte offset NP*128 - 2*lane
+    // Flag word of the pixel at cs / ds: the slot after the planes of its
+    // tile, uint16 per lane (byte offset NP*128 - 2*lane from the plane-0
+    // word).  Derived on use -- holding two more pointers costs spills.
     __device__ __forceinline__ uint16_t* cflag() const {
         const unsigned lane = threadIdx.x % kBlockPx;
         return reinterpret_cast<uint16_t*>(reinterpret_cast<char*>(cs) + bank_planes(MC, 3) * 128 - 2 * lane);
@@ -429,10 +413,6 @@ struct PixAddr {
         const unsigned lane = threadIdx.x % kBlockPx;
         return reinterpret_cast<uint16_t*>(reinterpret_cast<char*>(ds) + bank_planes(MD, 1) * 128 - 2 * lane);
     }
-#else
-    __device__ __forceinline__ uint16_t* cflag() const { return cfl; }
-    __device__ __forceinline__ uint16_t* dflag() const { return dfl; }
-#endif
 };
 
 // K1 after the first load round: the touched-prefix dispatch, the depth
@@ -470,18 +450,7 @@ __device__ __forceinline__ void fused_core(const FusedArgs& a, size_t i0, unsign
 
     // ---- colour stream (segment_color) ----
     const float vc[3] = {r.vc[0], r.vc[1], r.vc[2]};
-#if RGBDSEG_PRE_COLOR_L1
-    Mixture<kPre, 3> cpre;  // L1 hits (prefetched with the first round)
-#pragma unroll
-    for (int q = 0; q < kPre; ++q) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) cpre.mu[q][c] = p.cs[(q * 3 + c) * kBlockPx];
-        cpre.var[q] = p.cs[(MC * 3 + q) * kBlockPx];
-        cpre.w[q] = p.cs[(MC * 4 + q) * kBlockPx];
-    }
-#else
     const Mixture<kPre, 3>& cpre = r.cpre;
-#endif
     uint32_t cf1 = r.cf;
     bool replay = false;
     uint32_t lc =
@@ -490,13 +459,8 @@ __device__ __forceinline__ void fused_core(const FusedArgs& a, size_t i0, unsign
     if (cf1 != r.cf) st_h<kElide>(p.cflag(), (uint16_t)cf1);
 
     // ---- List-1 fusion on the registered depth mask ----
-#if RGBDSEG_LATE_FUSION
-    const uint32_t out0 = a.fuse ? a.out[i0 + t] : 0u;
+    const uint32_t out0 = a.fuse ? a.out[i0 + t] : 0u;  // L1 hits (plain loads)
     const int cpt0 = a.fuse ? (int)a.cpt[i0 + t] : 0;
-#else
-    const uint32_t out0 = r.out0;
-    const int cpt0 = r.cpt0;
-#endif
     uint32_t out = out0;
     int cpt = cpt0;
     if (a.fuse) {
@@ -524,28 +488,11 @@ __device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i0, unsig
     r.raw = ld_h<kElide>(a.d + i0 + t);
     r.cf = ld_h<kElide>(p.cflag());
     r.df = ld_h<kElide>(p.dflag());
-#if RGBDSEG_LATE_FUSION
-    if (a.fuse) {  // into L1 now, read at List 1
+    if (a.fuse) {  // fusion state into L1 now (no registers held), read at List 1
         asm volatile("prefetch.global.L1 [%0];" ::"l"(a.out + i0 + t));
         asm volatile("prefetch.global.L1 [%0];" ::"l"(a.cpt + i0 + t));
     }
-#else
-    r.out0 = a.fuse ? ld_h<kElide>(a.out + i0 + t) : 0u;
-    r.cpt0 = a.fuse ? (int)ld_h<kElide>(a.cpt + i0 + t) : 0;
-#endif
-#if RGBDSEG_PRE_COLOR_L1
-    // colour components 0..kPre-1 into L1 now, into registers at the colour step
-#pragma unroll
-    for (int q = 0; q < kPre; ++q) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(p.cs + (q * 3 + c) * kBlockPx));
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(p.cs + (MC * 3 + q) * kBlockPx));
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(p.cs + (MC * 4 + q) * kBlockPx));
-    }
-#else
     load_mix<MC, kElide>(p.cs, r.cpre);
-#endif
     load_mix<MD, kElide>(p.ds, r.dpre);
     fused_core<MC, MD, kElide>(a, i0, t, p, r, lab);
 }
