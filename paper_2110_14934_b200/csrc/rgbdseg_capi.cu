@@ -859,6 +859,7 @@ static int submit_unregistered(rgbdseg_processor* p, const uint8_t* r, const uin
         if (int rc = stage_in(gt, n, p->u_gt, &dgt, st)) return rc;
         const uint8_t* preds[3] = {rgbm, depm, p->fusion->out};
         CU(launch_confusion(preds, 3, (const uint8_t*)dgt, n, (size_t)w * h, dcounts, st));
+        CU(launch_counts_tn(dcounts, S, 3, (size_t)w * h, st));
     }
     if (fused_out && !fcopy) CU(cudaMemcpyAsync(fused_out, p->fusion->out, n, cudaMemcpyDefault, st));
     if (rgb_out) CU(cudaMemcpyAsync(rgb_out, rgbm, n, cudaMemcpyDefault, st));
@@ -914,7 +915,10 @@ static int submit_impl(rgbdseg_processor* p, const uint8_t* r, const uint8_t* g,
         a.n = p->npx;
         a.gt = gt;
         CU(launch_fused(a, p->variant, p->cs[0]));
-        if (gt) CU(cudaMemcpyAsync(counts_out, dcounts, ncnt * 8, cudaMemcpyDefault, p->cs[0]));
+        if (gt) {
+            CU(launch_counts_tn(dcounts, p->cfg.streams, 3, a.stream_px, p->cs[0]));
+            CU(cudaMemcpyAsync(counts_out, dcounts, ncnt * 8, cudaMemcpyDefault, p->cs[0]));
+        }
         ++p->frames;
         return RGBDSEG_OK;
     }
@@ -971,6 +975,8 @@ static int submit_impl(rgbdseg_processor* p, const uint8_t* r, const uint8_t* g,
     if (gt) {  // join both streams' counters, then copy them out
         CU(cudaEventRecord(p->ev[1], p->cs[1]));
         CU(cudaStreamWaitEvent(p->cs[0], p->ev[1], 0));
+        CU(launch_counts_tn(dcounts, p->cfg.streams, 3,
+                            (size_t)p->cfg.width * p->cfg.height, p->cs[0]));
         CU(cudaMemcpyAsync(counts_out, dcounts, ncnt * 8, cudaMemcpyDefault, p->cs[0]));
     }
     ++p->frames;
@@ -1017,6 +1023,7 @@ int rgbdseg_confusion_counts(const uint8_t* pred, const uint8_t* gt, size_t npx,
     const uint8_t* preds[1] = {(const uint8_t*)dp};
     CU(launch_confusion(preds, 1, (const uint8_t*)dg, npx, npx / streams,
                         static_cast<unsigned long long*>(c), 0));
+    CU(launch_counts_tn(static_cast<unsigned long long*>(c), streams, 1, npx / streams, 0));
     CU(cudaMemcpyAsync(counts, c, (size_t)streams * 4 * 8, cudaMemcpyDefault, 0));
     CU(cudaStreamSynchronize(0));
     return RGBDSEG_OK;

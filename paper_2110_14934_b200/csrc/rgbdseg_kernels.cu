@@ -288,64 +288,51 @@ __device__ __forceinline__ uint32_t k1_bank_pixel(float* s, const Mixture<(P > 0
 }
 
 // ---------------------------------------------------------------- evaluation
-// Per-stream confusion counts of up to 3 methods in one block: each warp
-// popcounts ballots, warps add into shared slots for the (at most two)
-// streams a block (kThreads pixels) can touch when streams hold >= kThreads pixels, and
-// one thread per nonzero counter adds it to the global int64 counters; a
-// warp whose pixels fall in another stream adds directly.  tn is derived
-// from the counted pixels: eval.cpp:17-28 assigns every pixel exactly one.
+// Per-stream confusion counts of up to 3 methods (eval.cpp:11-31) without
+// shared memory or block barriers: a warp whose pixels lie in one stream
+// turns two ballots per method into TP / FP / FN and lanes 0..3*NM-1 each add
+// one nonzero counter (most warps: none); a warp straddling two streams adds
+// per pixel.  TN is not counted here: eval.cpp:17-28 assigns every pixel
+// exactly one class, so k_counts_tn sets TN = pixels - TP - FP - FN once the
+// frame's launches are done.
 template <int NM>
 __device__ __forceinline__ void eval_accumulate(bool active, size_t j, size_t stream_px,
                                                 const uint32_t (&pred)[NM], uint32_t gt,
                                                 unsigned long long* counts) {
-    __shared__ unsigned int part[2][NM][4];
-    __shared__ unsigned long long s0;
-    const int tid = threadIdx.x;
-    const unsigned lane = tid & 31;
+    const unsigned lane = threadIdx.x & 31;
     const size_t s = active ? j / stream_px : ~size_t(0);
-    if (tid < 2 * NM * 4) (&part[0][0][0])[tid] = 0u;
-    if (tid == 0) s0 = s;  // thread 0 of a launched block is always active
-    __syncthreads();
-    const size_t base_s = s0;
-    const size_t s_lane0 = __shfl_sync(0xffffffffu, s, 0);
-    const bool uniform = __all_sync(0xffffffffu, !active || s == s_lane0);
+    const unsigned act = __ballot_sync(0xffffffffu, active);
+    if (!act) return;
+    const size_t s0 = __shfl_sync(0xffffffffu, s, __ffs(act) - 1);
+    const bool uniform = __all_sync(0xffffffffu, !active || s == s0);
     if (uniform) {
-        const unsigned act = __ballot_sync(0xffffffffu, active);
+        const unsigned g1 = __ballot_sync(0xffffffffu, active && gt);
+        unsigned v = 0u;
+        int slot = 0;
 #pragma unroll
         for (int m = 0; m < NM; ++m) {
             const unsigned p1 = __ballot_sync(0xffffffffu, active && pred[m]);
-            const unsigned g1 = __ballot_sync(0xffffffffu, active && gt);
-            const unsigned tp = __popc(p1 & g1), fp = __popc(p1 & ~g1), fn = __popc(~p1 & g1 & act);
-            const unsigned tn = __popc(act) - tp - fp - fn;
-            if (lane == 0 && act) {
-                const size_t slot = s_lane0 - base_s;
-                if (slot < 2) {
-                    atomicAdd(&part[slot][m][0], tp);
-                    atomicAdd(&part[slot][m][1], fp);
-                    atomicAdd(&part[slot][m][2], tn);
-                    atomicAdd(&part[slot][m][3], fn);
-                } else {
-                    unsigned long long* c = counts + (s_lane0 * NM + m) * 4;
-                    atomicAdd(c + 0, (unsigned long long)tp);
-                    atomicAdd(c + 1, (unsigned long long)fp);
-                    atomicAdd(c + 2, (unsigned long long)tn);
-                    atomicAdd(c + 3, (unsigned long long)fn);
-                }
-            }
+            const unsigned tp = __popc(p1 & g1), fp = __popc(p1 & ~g1), fn = __popc(~p1 & g1);
+            if (lane == 3 * m + 0) { v = tp; slot = m * 4 + 0; }
+            if (lane == 3 * m + 1) { v = fp; slot = m * 4 + 1; }
+            if (lane == 3 * m + 2) { v = fn; slot = m * 4 + 3; }
         }
-    } else if (active) {  // tiny streams: per-pixel atomics
+        if (lane < 3 * NM && v) atomicAdd(counts + s0 * NM * 4 + slot, (unsigned long long)v);
+    } else if (active) {  // warp across a stream boundary: per-pixel atomics
 #pragma unroll
         for (int m = 0; m < NM; ++m) {
             const int k = pred[m] ? (gt ? 0 : 1) : (gt ? 3 : 2);
-            atomicAdd(counts + (s * NM + m) * 4 + k, 1ull);
+            if (k != 2) atomicAdd(counts + (s * NM + m) * 4 + k, 1ull);
         }
     }
-    __syncthreads();
-    if (tid < 2 * NM * 4) {
-        const unsigned v = (&part[0][0][0])[tid];
-        const int slot = tid / (NM * 4);
-        if (v) atomicAdd(counts + (base_s + slot) * NM * 4 + (tid % (NM * 4)), (unsigned long long)v);
-    }
+}
+
+// TN of every (stream, method) counter: the pixels not counted as TP/FP/FN.
+__global__ void k_counts_tn(unsigned long long* counts, int n, unsigned long long stream_px) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    unsigned long long* c = counts + (size_t)i * 4;
+    c[2] = stream_px - c[0] - c[1] - c[3];
 }
 
 __global__ void __launch_bounds__(kThreads)
@@ -503,6 +490,8 @@ __global__ void __launch_bounds__(kThreads, RGBDSEG_FUSED_MIN_BLOCKS(kElide))
     const size_t i0 = (size_t)blockIdx.x * kThreads;
     const size_t i = i0 + threadIdx.x;
     const bool active = i < a.n;
+    if (a.gt && active)  // ground truth into L1 now, read after the steps
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(a.gt + i));
     if (!kElide && a.ahead && (threadIdx.x & 31) == 0) {
         // One bulk L2 prefetch per bank of the warp that starts about one
         // occupancy wave later: tiled blocks are contiguous, so its whole
@@ -521,7 +510,7 @@ __global__ void __launch_bounds__(kThreads, RGBDSEG_FUSED_MIN_BLOCKS(kElide))
     uint32_t lab[3] = {0u, 0u, 0u};
     if (active) fused_pixel<MC, MD, kElide>(a, i0, threadIdx.x, lab);
     if (a.gt) {  // evaluation epilogue: the masks never leave registers
-        const uint32_t g = active ? (uint32_t)ld_stream(a.gt + i) : 0u;
+        const uint32_t g = active ? (uint32_t)a.gt[i] : 0u;
         eval_accumulate<3>(active, a.base + i, a.stream_px, lab, g, a.counts);
     }
 }
@@ -1026,6 +1015,15 @@ cudaError_t launch_dilate(const uint8_t* in, uint8_t* tmp, uint8_t* out, int w, 
     cudaError_t e = go(k_dilate_pass<true>, n, s, in, tmp, w, h, n, radius);
     if (e != cudaSuccess) return e;
     return go(k_dilate_pass<false>, n, s, (const uint8_t*)tmp, out, w, h, n, radius);
+}
+
+cudaError_t launch_counts_tn(unsigned long long* counts, int streams, int methods,
+                            size_t stream_px, cudaStream_t s) {
+    const int n = streams * methods;
+    if (n <= 0) return cudaSuccess;
+    k_counts_tn<<<(n + 127) / 128, 128, 0, s>>>(counts, n, (unsigned long long)stream_px);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_confusion(const uint8_t* const* preds, int methods, const uint8_t* gt,

@@ -165,6 +165,11 @@ cudaError_t launch_confusion(const uint8_t* const* preds, int methods, const uin
                              size_t npx, size_t stream_px, unsigned long long* counts,
                              cudaStream_t s);
 
+// TN = stream_px - TP - FP - FN for counts[streams][methods][tp, fp, tn, fn]
+// (the kernels above count TP / FP / FN only); run after a frame's launches.
+cudaError_t launch_counts_tn(unsigned long long* counts, int streams, int methods,
+                            size_t stream_px, cudaStream_t s);
+
 uint64_t launches();
 
 }  // namespace rgbdseg_b200
