@@ -637,6 +637,49 @@ __global__ void k_bank_scatter(BankView bk, int plane, size_t n, const void* src
 }
 
 // ---------------------------------------------------------------- K1c fusion
+// k_fuse on 16 pixels per thread (16-byte-aligned planes; the launcher
+// checks, and the last partial chunk goes per pixel).
+__global__ void __launch_bounds__(kThreads)
+    k_fuse16(uint8_t* __restrict__ out, int8_t* __restrict__ cpt, const uint8_t* __restrict__ rgb,
+             const uint8_t* __restrict__ dep, uint8_t* __restrict__ out_copy, int limit, size_t n) {
+    const size_t c = (size_t)blockIdx.x * kThreads + threadIdx.x;
+    const size_t j0 = c * 16;
+    if (j0 >= n) return;
+    if (j0 + 16 > n) {
+        for (size_t j = j0; j < n; ++j) {
+            uint32_t o = out[j];
+            int k = cpt[j];
+            fuse_pixel(rgb[j], dep[j], limit, o, k);
+            out[j] = (uint8_t)o;
+            cpt[j] = (int8_t)k;
+            if (out_copy) out_copy[j] = (uint8_t)o;
+        }
+        return;
+    }
+    const uint4 vr = reinterpret_cast<const uint4*>(rgb)[c], vd = reinterpret_cast<const uint4*>(dep)[c];
+    const uint4 vo = reinterpret_cast<const uint4*>(out)[c];
+    const uint4 vc = reinterpret_cast<const uint4*>(cpt)[c];
+    const uint32_t R[4] = {vr.x, vr.y, vr.z, vr.w}, D[4] = {vd.x, vd.y, vd.z, vd.w};
+    uint32_t O[4] = {vo.x, vo.y, vo.z, vo.w}, K[4] = {vc.x, vc.y, vc.z, vc.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        uint32_t no = 0u, nk = 0u;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            uint32_t o = (O[q] >> (8 * b)) & 0xffu;
+            int k = (int)(int8_t)((K[q] >> (8 * b)) & 0xffu);
+            fuse_pixel((R[q] >> (8 * b)) & 0xffu, (D[q] >> (8 * b)) & 0xffu, limit, o, k);
+            no |= (o & 0xffu) << (8 * b);
+            nk |= ((uint32_t)k & 0xffu) << (8 * b);
+        }
+        O[q] = no;
+        K[q] = nk;
+    }
+    reinterpret_cast<uint4*>(out)[c] = make_uint4(O[0], O[1], O[2], O[3]);
+    reinterpret_cast<uint4*>(cpt)[c] = make_uint4(K[0], K[1], K[2], K[3]);
+    if (out_copy) reinterpret_cast<uint4*>(out_copy)[c] = make_uint4(O[0], O[1], O[2], O[3]);
+}
+
 __global__ void __launch_bounds__(kThreads)
     k_fuse(uint8_t* __restrict__ out, int8_t* __restrict__ cpt, const uint8_t* __restrict__ rgb,
            const uint8_t* __restrict__ dep, uint8_t* __restrict__ out_copy, int limit, size_t n) {
@@ -816,17 +859,13 @@ __global__ void k_render(const __grid_constant__ SceneFrame sc, uint8_t* R, uint
 // register_mask (registration.cpp:50-78): the same fp64 expression trees,
 // every op an explicit round-to-nearest double intrinsic (no contraction),
 // lround() half away from zero like std::lround.
-__global__ void k_register_splat(const uint8_t* __restrict__ mask,
-                                 const uint16_t* __restrict__ depth, int dw, int dh, size_t n,
-                                 const __grid_constant__ RigDev rig, int cw, int ch,
-                                 uint8_t* __restrict__ out) {
-    const size_t idx = (size_t)blockIdx.x * kThreads + threadIdx.x;
-    if (idx >= n) return;
+__device__ __forceinline__ void splat_pixel(size_t idx, const uint16_t* __restrict__ depth,
+                                            int dw, int dh, const RigDev& rig, int cw, int ch,
+                                            uint8_t* __restrict__ out) {
     const size_t per = (size_t)dw * dh;
     const size_t s = idx / per;
     const int p = (int)(idx - s * per);
     const int u = p % dw, v = p / dw;
-    if (!mask[idx]) return;
     const uint32_t raw = depth[idx];
     if (raw == 0) return;  // no range return, cannot be registered
     const double z = __dmul_rn((double)raw, rig.scale);
@@ -844,6 +883,34 @@ __global__ void k_register_splat(const uint8_t* __restrict__ mask,
     const long vc = lround(__dadd_rn(__ddiv_rn(__dmul_rn(rig.cfy, yc), zc), rig.ccy));
     if (uc < 0 || uc >= cw || vc < 0 || vc >= ch) return;
     out[s * (size_t)cw * ch + (size_t)vc * cw + uc] = 1;
+}
+
+__global__ void k_register_splat(const uint8_t* __restrict__ mask,
+                                 const uint16_t* __restrict__ depth, int dw, int dh, size_t n,
+                                 const __grid_constant__ RigDev rig, int cw, int ch,
+                                 uint8_t* __restrict__ out) {
+    const size_t idx = (size_t)blockIdx.x * kThreads + threadIdx.x;
+    if (idx >= n || !mask[idx]) return;
+    splat_pixel(idx, depth, dw, dh, rig, cw, ch, out);
+}
+
+// 16 mask bytes per thread (one 16-byte load; most chunks are background
+// and stop there).  n % 16 == 0 and a 16-byte-aligned mask (launcher checks).
+__global__ void k_register_splat16(const uint8_t* __restrict__ mask,
+                                   const uint16_t* __restrict__ depth, int dw, int dh, size_t n16,
+                                   const __grid_constant__ RigDev rig, int cw, int ch,
+                                   uint8_t* __restrict__ out) {
+    const size_t c = (size_t)blockIdx.x * kThreads + threadIdx.x;
+    if (c >= n16) return;
+    const uint4 m = reinterpret_cast<const uint4*>(mask)[c];
+    const uint32_t wds[4] = {m.x, m.y, m.z, m.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if (!wds[k]) continue;
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+            if ((wds[k] >> (8 * b)) & 0xffu) splat_pixel(c * 16 + k * 4 + b, depth, dw, dh, rig, cw, ch, out);
+    }
 }
 
 // dilate_mask (registration.cpp:33-48): OR over a clipped (2r+1)-square,
@@ -866,6 +933,54 @@ __global__ void k_dilate_pass(const uint8_t* __restrict__ in, uint8_t* __restric
         for (int yy = y0; yy <= y1 && !acc; ++yy) acc |= in[base + (size_t)yy * w + x];
     }
     out[idx] = acc ? 1 : 0;
+}
+
+// Vector forms of the two passes: 16 pixels of one row per thread (w % 16
+// == 0, 16-byte-aligned planes).  Bytes are OR-ed as 0 / nonzero and the
+// result normalised to 0 / 1 with a per-byte compare (__vcmpne4).
+__device__ __forceinline__ uint32_t nz01(uint32_t v) { return __vcmpne4(v, 0u) & 0x01010101u; }
+
+// Column pass: OR of the clipped rows y-r..y+r.
+__global__ void k_dilate_cols16(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int w,
+                                int h, size_t n16, int r) {
+    const size_t c = (size_t)blockIdx.x * kThreads + threadIdx.x;
+    if (c >= n16) return;
+    const size_t idx = c * 16, per = (size_t)w * h;
+    const size_t base = (idx / per) * per;
+    const int p = (int)(idx - base), x = p % w, y = p / w;
+    const int y0 = max(0, y - r), y1 = min(h - 1, y + r);
+    uint4 acc = make_uint4(0u, 0u, 0u, 0u);
+    for (int yy = y0; yy <= y1; ++yy) {
+        const uint4 v = *reinterpret_cast<const uint4*>(in + base + (size_t)yy * w + x);
+        acc.x |= v.x;
+        acc.y |= v.y;
+        acc.z |= v.z;
+        acc.w |= v.w;
+    }
+    *reinterpret_cast<uint4*>(out + idx) = make_uint4(nz01(acc.x), nz01(acc.y), nz01(acc.z), nz01(acc.w));
+}
+
+// Row pass (r <= 16): the chunk and its clipped neighbours as a 48-byte
+// window; output byte i = OR of window bytes 16+i-r .. 16+i+r, built from
+// byte-shifted words (funnel shifts).
+__global__ void k_dilate_rows16(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int w,
+                                size_t n16, int r) {
+    const size_t c = (size_t)blockIdx.x * kThreads + threadIdx.x;
+    if (c >= n16) return;
+    const size_t idx = c * 16;
+    const int x = (int)(idx % (size_t)w);
+    const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+    const uint4 L = x > 0 ? *reinterpret_cast<const uint4*>(in + idx - 16) : z;
+    const uint4 Mv = *reinterpret_cast<const uint4*>(in + idx);
+    const uint4 Rv = x + 16 < w ? *reinterpret_cast<const uint4*>(in + idx + 16) : z;
+    const uint32_t wd[13] = {L.x, L.y, L.z, L.w, Mv.x, Mv.y, Mv.z, Mv.w, Rv.x, Rv.y, Rv.z, Rv.w, 0u};
+    uint32_t acc[4] = {0u, 0u, 0u, 0u};
+    for (int d = -r; d <= r; ++d) {
+        const int o = 16 + d, q = o >> 2, sh = 8 * (o & 3);  // window starts at byte o
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[j] |= __funnelshift_r(wd[q + j], wd[q + j + 1], sh);
+    }
+    *reinterpret_cast<uint4*>(out + idx) = make_uint4(nz01(acc[0]), nz01(acc[1]), nz01(acc[2]), nz01(acc[3]));
 }
 
 template <typename K, typename... Args>
@@ -974,8 +1089,12 @@ cudaError_t launch_bank_scatter(BankView bk, int plane, size_t n, const void* sr
     return go(k_bank_scatter, n, s, bk, plane, n, src);
 }
 
+inline bool al16(const void* p) { return ((uintptr_t)p & 15u) == 0u; }
+
 cudaError_t launch_fuse(uint8_t* out, int8_t* cpt, const uint8_t* rgb, const uint8_t* dep,
                         uint8_t* out_copy, int limit, size_t n, cudaStream_t s) {
+    if (al16(out) && al16(cpt) && al16(rgb) && al16(dep) && (!out_copy || al16(out_copy)))
+        return go(k_fuse16, (n + 15) / 16, s, out, cpt, rgb, dep, out_copy, limit, n);
     return go(k_fuse, n, s, out, cpt, rgb, dep, out_copy, limit, n);
 }
 
@@ -1002,6 +1121,8 @@ cudaError_t launch_register_splat(const uint8_t* mask, const uint16_t* depth, in
                                   int streams, const RigDev& rig, int cw, int ch, uint8_t* out,
                                   cudaStream_t s) {
     const size_t n = (size_t)dw * dh * streams;
+    if (n % 16 == 0 && al16(mask))
+        return go(k_register_splat16, n / 16, s, mask, depth, dw, dh, n / 16, rig, cw, ch, out);
     return go(k_register_splat, n, s, mask, depth, dw, dh, n, rig, cw, ch, out);
 }
 
@@ -1011,6 +1132,12 @@ cudaError_t launch_dilate(const uint8_t* in, uint8_t* tmp, uint8_t* out, int w, 
     if (radius <= 0) {  // dilate_mask returns the mask unchanged
         if (out == in) return cudaSuccess;
         return cudaMemcpyAsync(out, in, n, cudaMemcpyDeviceToDevice, s);
+    }
+    if (w % 16 == 0 && al16(in) && al16(tmp) && al16(out)) {
+        cudaError_t e = radius <= 16 ? go(k_dilate_rows16, n / 16, s, in, tmp, w, n / 16, radius)
+                                     : go(k_dilate_pass<true>, n, s, in, tmp, w, h, n, radius);
+        if (e != cudaSuccess) return e;
+        return go(k_dilate_cols16, n / 16, s, (const uint8_t*)tmp, out, w, h, n / 16, radius);
     }
     cudaError_t e = go(k_dilate_pass<true>, n, s, in, tmp, w, h, n, radius);
     if (e != cudaSuccess) return e;

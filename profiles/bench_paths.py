@@ -102,7 +102,9 @@ def main():
     ap.add_argument("--streams", type=int, default=64)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--rows", default="unregistered,eval_epilogue,augmented4")
     args = ap.parse_args()
+    rows = set(args.rows.split(","))
     S, n = args.streams, args.steps + args.warmup
     cfg = R.RunConfig.defaults()
     cfg.color_gmm.components = cfg.depth_gmm.components = M
@@ -110,6 +112,15 @@ def main():
     torch.cuda.synchronize()
 
     # ---- unregistered: K1 (masks) + splat + dilation + fuse ------------------
+    if "unregistered" in rows:
+        unregistered(args, S, cfg, fr)
+    if "eval_epilogue" in rows:
+        eval_epilogue(args, S, n, cfg, fr)
+    if "augmented4" in rows:
+        augmented4(args, S, n, cfg, fr)
+
+
+def unregistered(args, S, cfg, fr):
     proc = R.SequenceProcessor(W, H, cfg, streams=S, registered=False, rig=rig())
     preroll(proc, S)
     ms = timed(proc, args.steps, args.warmup,
@@ -122,7 +133,9 @@ def main():
           "timing": "CUDA events on the processor stream"})
     del proc
 
-    # ---- evaluation epilogue: fused K1 with and without ground truth ---------
+
+def eval_epilogue(args, S, n, cfg, fr):
+    """Fused K1 with and without ground truth."""
     proc = R.SequenceProcessor(W, H, cfg, streams=S)
     preroll(proc, S)
     # pinned, so the per-frame counts read-back stays asynchronous
@@ -145,7 +158,9 @@ def main():
           "timing": "CUDA events on the processor stream"})
     del proc
 
-    # ---- Augmented4 bank ------------------------------------------------------
+
+def augmented4(args, S, n, cfg, fr):
+    """ModelBank(Augmented4) + segment_augmented."""
     bank = R.ModelBank(W, H, "Augmented4", cfg.color_gmm, streams=S)
     resc = R.DepthRescale(0.0, 4000.0)
     mask = torch.empty((S, H, W), dtype=torch.uint8, device="cuda")

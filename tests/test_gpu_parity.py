@@ -1104,3 +1104,53 @@ def test_config4_four_vga_streams_300_frames_vs_reference(R, cuda):
         for s in range(S):
             assert P[:, s * n:(s + 1) * n].tobytes() == refs[s].bank_planes(which).tobytes(), s
             assert np.array_equal(fl[s * n:(s + 1) * n], refs[s].flags(which)), s
+
+
+@pytest.mark.parametrize("w", [96, 128, 83])
+def test_dilate_vector_paths_match_oracle(R, port, w):
+    """The 16-pixel-per-thread passes (w % 16 == 0; radius <= 16 for the row
+    pass, the per-pixel row pass beyond) against the oracle, streams of
+    several frames included through the unregistered processor below."""
+    rng = np.random.default_rng(w)
+    h = 45
+    for r in (0, 1, 2, 5, 15, 16, 17):
+        m = (rng.random((h, w)) < 0.04).astype(np.uint8)
+        m[0, 0] = m[h - 1, w - 1] = m[h // 2, 15] = m[h // 2, 16] = 1
+        exp = np.empty_like(m)
+        port.lib.orc_dilate(m, exp, w, h, r)
+        assert np.array_equal(R.dilate_mask(m, r), exp), r
+
+
+def test_register_vector_path_matches_oracle(R, port):
+    """k_register_splat16 (16 mask bytes per thread) at widths divisible by
+    16, dense and sparse masks, against the oracle."""
+    from helpers import random_rig
+    from test_oracle import _port_register
+
+    rng = np.random.default_rng(71)
+    for trial, (w, h) in enumerate([(64, 48), (160, 120), (640, 480), (48, 16)]):
+        a = random_rig(rng, w, h, big=trial % 2 == 1)
+        for density in (0.02, 0.6):
+            mask = (rng.random((h, w)) < density).astype(np.uint8)
+            depth = rng.integers(0, 5000, (h, w)).astype(np.uint16)
+            depth[rng.random((h, w)) < 0.1] = 0
+            got = R.register_mask(mask, depth, _rig_from_array(R, a), dilation_radius=trial % 3)
+            assert np.array_equal(got, _port_register(port, mask, depth, a, w, h, trial % 3)), (w, density)
+
+
+def test_fusion_vector_path_with_partial_chunk(R, port):
+    """k_fuse16 over n = 16k + 7 pixels (the last chunk per pixel) against
+    the oracle's List 1, 30 random steps."""
+    rng = np.random.default_rng(8)
+    n = 16 * 257 + 7
+    fs = R.FusionState(n, 1, initial_label=1, counter_limit=3)
+    out = np.empty(n, np.uint8)
+    cpt = np.empty(n, np.int8)
+    port.lib.orc_fusion_reset(out, cpt, n, 1)
+    for step in range(30):
+        r = (rng.random(n) < 0.5).astype(np.uint8)
+        d = (rng.random(n) < 0.5).astype(np.uint8)
+        got = fs.step(r.reshape(1, -1), d.reshape(1, -1))
+        port.lib.orc_fuse(out, cpt, n, 3, r, d)
+        assert np.array_equal(got.ravel(), out), step
+        assert np.array_equal(fs.cpt.ravel(), cpt), step
