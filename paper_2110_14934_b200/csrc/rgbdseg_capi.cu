@@ -454,7 +454,7 @@ int rgbdseg_segment_color(rgbdseg_bank* b, const uint8_t* r, const uint8_t* g, c
             dm = static_cast<uint8_t*>(p);
         }
     }
-    CU(launch_bank_color(b->view(*cfg), to_k(*cfg), (const uint8_t*)dr, (const uint8_t*)dg,
+    CU(launch_bank_color(b->view(*cfg), to_k(*cfg, b->vvar), (const uint8_t*)dr, (const uint8_t*)dg,
                          (const uint8_t*)db, dm, b->npx, b->stream));
     return finish_mask(dm, mask_out, b->npx, b->stream);
 }
@@ -475,7 +475,7 @@ int rgbdseg_segment_depth(rgbdseg_bank* b, const uint16_t* depth_mm,
             dm = static_cast<uint8_t*>(p);
         }
     }
-    CU(launch_bank_depth(b->view(*cfg), to_k(*cfg), (const uint16_t*)dd, dm, b->npx, b->stream));
+    CU(launch_bank_depth(b->view(*cfg), to_k(*cfg, b->vvar), (const uint16_t*)dd, dm, b->npx, b->stream));
     return finish_mask(dm, mask_out, b->npx, b->stream);
 }
 
@@ -500,7 +500,7 @@ int rgbdseg_segment_augmented(rgbdseg_bank* b, const uint8_t* r, const uint8_t* 
             dm = static_cast<uint8_t*>(p);
         }
     }
-    CU(launch_bank_aug(b->view(*cfg), to_k(*cfg), (const uint8_t*)dr, (const uint8_t*)dg,
+    CU(launch_bank_aug(b->view(*cfg), to_k(*cfg, b->vvar), (const uint8_t*)dr, (const uint8_t*)dg,
                        (const uint8_t*)db, (const uint16_t*)dd, min_mm, max_mm, dm, b->npx,
                        b->stream));
     return finish_mask(dm, mask_out, b->npx, b->stream);

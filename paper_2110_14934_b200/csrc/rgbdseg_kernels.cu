@@ -173,35 +173,6 @@ __device__ __forceinline__ void store_mix_elide(float* s, const Mixture<N, C>& m
             st_h<H>(s + (L * C + L + i) * kBlockPx, m.w[i]);
 }
 
-// run_bank's per-pixel body (segmenter.cpp:80-96) on a mixture loaded from
-// `src` (K1b).  The branch-free fast step runs first; a pixel whose operands
-// leave its exact ranges (gmm_pixel.cuh) is reloaded and replayed by the
-// generic step, so the result is bit-identical either way.
-template <int M, int C>
-__device__ __forceinline__ uint32_t bank_pixel(Mixture<M, C>& m, const float* src,
-                                               const float (&v)[C], bool initialised,
-                                               const MixCfg& k, int& touched) {
-    if (!initialised) {
-        gmm_init(m, v, k);
-        touched = -1;
-        return 0u;
-    }
-    bool ok = k.fast != 0;
-    uint32_t label = gmm_step_fast(m, v, k, touched, ok);
-    if (!ok) {
-        load_mix<M>(src, m);
-        label = gmm_step(m, v, k, touched);
-    }
-    return label;
-}
-
-// K1's step of one initialised pixel on components 0..N-1 of a bank of M.
-// Components N..M-1 are untouched for this pixel: together with any
-// untouched ones below N they act exactly as the full mixture's untouched
-// tail (fitness +0, ranked after every other component in index order,
-// weight +0 through the update, the same band), so the step on N
-// components returns the full step's label and state.  The elided variant
-// reads only `need`; the dense one (N == M, need = all) rewrites everything.
 // Exact replay of a pixel the fast step refused: the whole mixture from
 // memory (nothing was stored) through the generic gmm_step.  K1 runs it once
 // per bank after both fast steps, so there is one inlined copy per bank
@@ -516,48 +487,53 @@ __global__ void __launch_bounds__(kThreads, RGBDSEG_FUSED_MIN_BLOCKS(kElide))
 }
 
 // ---------------------------------------------------------------- K1b banks
+// One bank alone (segment_color / segment_depth / segment_augmented drop-ins)
+// on K1's machinery: the flag word's untouched mask, the step on the warp's
+// touched prefix, components 0..P-1 read with the flag word, the exact
+// replay deferred, L2-only loads and write-back stores.  `step` false
+// (depth no-return) leaves the pixel untouched but joins the warp reduction.
+template <int M, int C, int P>
+__device__ __forceinline__ uint32_t bank_elided(const BankView& bk, size_t j, const float (&v)[C],
+                                                bool step, const MixCfg& k) {
+    float* s = px_base<M, C>(bk, j);
+    uint16_t* fl = px_flag<M, C>(bk, j);
+    const uint32_t f = ld_h<true>(fl);
+    Mixture<P, C> pre;
+    load_mix<M, true>(s, pre);
+    const unsigned am = __activemask();
+    const int Kw = __reduce_max_sync(am, (step && (f & 0xffu)) ? touched_prefix<M>(f) : 1);
+    if (!step) return 0u;
+    uint32_t f1 = f;
+    bool replay = false;
+    uint32_t lab = k1_bank_pixel<M, C, P, true>(s, pre, ~flag_untouched<M>(f), Kw, v, k, bk, f1,
+                                                replay);
+    if (replay) lab = replay_pixel<M, C, true>(s, v, k, bk, f1);
+    if (f1 != f) st_h<true>(fl, (uint16_t)f1);
+    return lab;
+}
+
 template <int M>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, RGBDSEG_FUSED_MIN_BLOCKS(true))
     k_bank_color(BankView bk, MixCfg k, const uint8_t* __restrict__ r,
                  const uint8_t* __restrict__ g, const uint8_t* __restrict__ b,
                  uint8_t* __restrict__ mask, size_t n) {
     const size_t j = (size_t)blockIdx.x * kThreads + threadIdx.x;
     if (j >= n) return;
-    const float v[3] = {(float)r[j], (float)g[j], (float)b[j]};
-    float* st = px_base<M, 3>(bk, j);
-    uint16_t* fl = px_flag<M, 3>(bk, j);
-    const uint32_t f = *fl;
-    Mixture<M, 3> m;
-    load_mix<M>(st, m);
-    int t;
-    const uint32_t lab = bank_pixel(m, st, v, (f & 0xffu) != 0, k, t);
-    store_mix<M>(st, m);
-    const uint32_t f1 = flag_after<M>(f, t, m.w, bk);
-    if (f1 != f) *fl = (uint16_t)f1;
+    const float v[3] = {(float)ld_h<true>(r + j), (float)ld_h<true>(g + j),
+                        (float)ld_h<true>(b + j)};
+    const uint32_t lab = bank_elided<M, 3, 2>(bk, j, v, true, k);
     if (mask) mask[j] = (uint8_t)lab;
 }
 
 template <int M>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, RGBDSEG_FUSED_MIN_BLOCKS(true))
     k_bank_depth(BankView bk, MixCfg k, const uint16_t* __restrict__ d,
                  uint8_t* __restrict__ mask, size_t n) {
     const size_t j = (size_t)blockIdx.x * kThreads + threadIdx.x;
     if (j >= n) return;
-    const uint32_t raw = d[j];
-    uint32_t lab = 0;
-    if (raw != 0) {  // segmenter.cpp:84,128
-        const float v[1] = {(float)raw};
-        float* st = px_base<M, 1>(bk, j);
-        uint16_t* fl = px_flag<M, 1>(bk, j);
-        const uint32_t f = *fl;
-        Mixture<M, 1> m;
-        load_mix<M>(st, m);
-        int t;
-        lab = bank_pixel(m, st, v, (f & 0xffu) != 0, k, t);
-        store_mix<M>(st, m);
-        const uint32_t f1 = flag_after<M>(f, t, m.w, bk);
-        if (f1 != f) *fl = (uint16_t)f1;
-    }
+    const uint32_t raw = ld_h<true>(d + j);
+    const float v[1] = {(float)raw};
+    const uint32_t lab = bank_elided<M, 1, 1>(bk, j, v, raw != 0, k);  // segmenter.cpp:84,128
     if (mask) mask[j] = (uint8_t)lab;
 }
 
@@ -572,25 +548,16 @@ __device__ __forceinline__ float rescale_depth(float d, float lo, float hi) {
 // (R, G, B, rescaled depth).  No no-return sentinel here: raw 0 rescales to
 // channel value 0 and is modelled like any other observation.
 template <int M>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, RGBDSEG_FUSED_MIN_BLOCKS(true))
     k_bank_aug(BankView bk, MixCfg k, const uint8_t* __restrict__ r,
                const uint8_t* __restrict__ g, const uint8_t* __restrict__ b,
                const uint16_t* __restrict__ d, float lo, float hi, uint8_t* __restrict__ mask,
                size_t n) {
     const size_t j = (size_t)blockIdx.x * kThreads + threadIdx.x;
     if (j >= n) return;
-    const float v[4] = {(float)r[j], (float)g[j], (float)b[j],
-                        rescale_depth((float)d[j], lo, hi)};
-    float* st = px_base<M, 4>(bk, j);
-    uint16_t* fl = px_flag<M, 4>(bk, j);
-    const uint32_t f = *fl;
-    Mixture<M, 4> m;
-    load_mix<M>(st, m);
-    int t;
-    const uint32_t lab = bank_pixel(m, st, v, (f & 0xffu) != 0, k, t);
-    store_mix<M>(st, m);
-    const uint32_t f1 = flag_after<M>(f, t, m.w, bk);
-    if (f1 != f) *fl = (uint16_t)f1;
+    const float v[4] = {(float)ld_h<true>(r + j), (float)ld_h<true>(g + j),
+                        (float)ld_h<true>(b + j), rescale_depth((float)ld_h<true>(d + j), lo, hi)};
+    const uint32_t lab = bank_elided<M, 4, 2>(bk, j, v, true, k);
     if (mask) mask[j] = (uint8_t)lab;
 }
 

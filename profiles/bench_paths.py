@@ -102,7 +102,7 @@ def main():
     ap.add_argument("--streams", type=int, default=64)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--rows", default="unregistered,eval_epilogue,augmented4")
+    ap.add_argument("--rows", default="unregistered,eval_epilogue,augmented4,bank_api")
     args = ap.parse_args()
     rows = set(args.rows.split(","))
     S, n = args.streams, args.steps + args.warmup
@@ -118,6 +118,48 @@ def main():
         eval_epilogue(args, S, n, cfg, fr)
     if "augmented4" in rows:
         augmented4(args, S, n, cfg, fr)
+    if "bank_api" in rows:
+        bank_api(args, S, n, cfg, fr)
+
+
+def wall(fn, steps):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for k in range(steps):
+        fn(k)
+    torch.cuda.synchronize()
+    return (time.perf_counter() - t0) * 1e3 / steps
+
+
+def bank_api(args, S, n, cfg, fr):
+    """The reference's unfused composition through the bank-level drop-in API
+    (segment_color / segment_depth / fuse_step, segmenter.cpp:107-131,
+    fusion.cpp:17-46), device frames and masks, each call synchronous."""
+    cb = R.ModelBank(W, H, "Color3", cfg.color_gmm, streams=S)
+    db = R.ModelBank(W, H, "Depth1", cfg.depth_gmm, streams=S)
+    fs = R.FusionState(W, H, streams=S)
+    rgb = torch.empty((S, H, W), dtype=torch.uint8, device="cuda")
+    dep = torch.empty_like(rgb)
+    fused = torch.empty_like(rgb)
+    for f in range(0, START):  # the same pre-roll as the processor rows
+        g = R.render_scenario("A", W, H, f, streams=S, seed0=1)
+        R.segment_color(cb, g["r"], g["g"], g["b"], cfg.color_gmm, out=rgb)
+        R.segment_depth(db, g["depth"], cfg.depth_gmm, out=dep)
+    for f in range(n):
+        R.segment_color(cb, fr[f]["r"], fr[f]["g"], fr[f]["b"], cfg.color_gmm, out=rgb)
+        R.segment_depth(db, fr[f]["depth"], cfg.depth_gmm, out=dep)
+    k0 = args.warmup
+    ms_c = wall(lambda k: R.segment_color(cb, fr[k0 + k]["r"], fr[k0 + k]["g"], fr[k0 + k]["b"],
+                                          cfg.color_gmm, out=rgb), args.steps)
+    ms_d = wall(lambda k: R.segment_depth(db, fr[k0 + k]["depth"], cfg.depth_gmm, out=dep),
+                args.steps)
+    ms_f = wall(lambda k: fs.step(rgb, dep, out=fused), args.steps)
+    line("segment_color", S, ms_c, 3 + 40 * M + 2 + 1,
+         {"kernels": "k_bank_color", "timing": "host wall clock around synchronous calls"})
+    line("segment_depth", S, ms_d, 2 + 24 * M + 2 + 1,
+         {"kernels": "k_bank_depth", "timing": "host wall clock around synchronous calls"})
+    line("fuse_step", S, ms_f, 7,
+         {"kernels": "k_fuse16", "timing": "host wall clock around synchronous calls"})
 
 
 def unregistered(args, S, cfg, fr):
