@@ -5,16 +5,22 @@
 //                    -> segment_color/segment_depth segmenter.cpp:107-131 ->
 //                    run_bank :70-99 -> step_pixel mixture.cpp:148-154 ->
 //                    fuse_step fusion.cpp:17-46).  Masks stay in registers.
-// K1b k_bank_*       one bank alone (segment_color / segment_depth drop-ins).
-// K1c k_fuse         fuse_step alone.
+// K1b k_bank_*       one bank alone (segment_color / segment_depth /
+//                    segment_augmented drop-ins), on K1's machinery.
+// K1c k_fuse16/_fuse fuse_step alone.
+// K2  k_register_splat16, k_dilate_rows16/cols16 (+ per-pixel fallbacks)
+//                    register_mask + dilate_mask (registration.cpp:33-78).
+// K4  k_confusion    confusion_counts (eval.cpp:11-31); K1 has it fused.
 // K0  k_mix_*        the per-pixel API (init_mixture / step_pixel) batched.
 // K3  k_render       synthetic scene generator (synthetic.cpp:119-195).
 //
-// All kernels are memory-bound elementwise work: one thread per pixel, the
-// mixture in registers for the whole update, structure-of-arrays planes in
-// HBM so every plane access of a warp is one fully coalesced 128-byte line.
-// Built with -fmad=false -prec-div=true -prec-sqrt=true -ftz=false and the
-// arithmetic spelled with explicit _rn intrinsics (gmm_pixel.cuh).
+// Elementwise work over HBM-resident state: one thread per pixel, the
+// mixture in registers for the whole update, a tiled structure-of-arrays
+// bank so every plane access of a warp is one coalesced 128-byte line, and
+// a per-pixel mask of untouched components so most of the state is never
+// read (rgbdseg_kernels.cuh).  Built with -fmad=false -prec-div=true
+// -prec-sqrt=true -ftz=false and the arithmetic spelled with explicit _rn
+// intrinsics (gmm_pixel.cuh).
 #include <algorithm>
 #include <atomic>
 #include <cstdlib>
@@ -324,7 +330,7 @@ __global__ void __launch_bounds__(kThreads)
 
 // ---------------------------------------------------------------- K1 fused
 // Resident 128-thread blocks per SM: the dense variant is HBM-bound at 6
-// (80 regs, 24 warps/SM); the elided one is issue/latency-bound and gains
+// (72 regs, 24 warps/SM); the elided one is issue/latency-bound and gains
 // from 12 (40 regs, 48 warps/SM) despite spills (profiles/variants_r01.json).
 #ifndef RGBDSEG_PRE_COLOR  // colour components loaded with the flag words (2 or 3)
 #define RGBDSEG_PRE_COLOR 2
