@@ -461,13 +461,15 @@ __device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i0, unsig
     fused_core<MC, MD, kElide>(a, i0, t, p, r, lab);
 }
 
-template <int MC, int MD, bool kElide>
+// kEval: with the evaluation epilogue (a.gt set).  A separate instantiation,
+// so the plain kernel's register allocation carries none of it (measured 6%).
+template <int MC, int MD, bool kElide, bool kEval>
 __global__ void __launch_bounds__(kThreads, RGBDSEG_FUSED_MIN_BLOCKS(kElide))
     k_fused_ldg(const __grid_constant__ FusedArgs a) {
     const size_t i0 = (size_t)blockIdx.x * kThreads;
     const size_t i = i0 + threadIdx.x;
     const bool active = i < a.n;
-    if (a.gt && active)  // ground truth into L1 now, read after the steps
+    if (kEval && active)  // ground truth into L1 now, read after the steps
         asm volatile("prefetch.global.L1 [%0];" ::"l"(a.gt + i));
     if (!kElide && a.ahead && (threadIdx.x & 31) == 0) {
         // One bulk L2 prefetch per bank of the warp that starts about one
@@ -486,7 +488,7 @@ __global__ void __launch_bounds__(kThreads, RGBDSEG_FUSED_MIN_BLOCKS(kElide))
     }
     uint32_t lab[3] = {0u, 0u, 0u};
     if (active) fused_pixel<MC, MD, kElide>(a, i0, threadIdx.x, lab);
-    if (a.gt) {  // evaluation epilogue: the masks never leave registers
+    if constexpr (kEval) {  // evaluation epilogue: the masks never leave registers
         const uint32_t g = active ? (uint32_t)a.gt[i] : 0u;
         eval_accumulate<3>(active, a.base + i, a.stream_px, lab, g, a.counts);
     }
@@ -967,10 +969,13 @@ cudaError_t go(K kernel, size_t n, cudaStream_t s, Args... args) {
 template <int MC, int MD>
 cudaError_t fused_ldg_md(const FusedArgs& a, bool elide, cudaStream_t s) {
     if (a.n == 0) return cudaSuccess;
+    const unsigned nb = blocks_for(a.n);
     if (elide)
-        k_fused_ldg<MC, MD, true><<<blocks_for(a.n), kThreads, 0, s>>>(a);
+        a.gt ? k_fused_ldg<MC, MD, true, true><<<nb, kThreads, 0, s>>>(a)
+             : k_fused_ldg<MC, MD, true, false><<<nb, kThreads, 0, s>>>(a);
     else
-        k_fused_ldg<MC, MD, false><<<blocks_for(a.n), kThreads, 0, s>>>(a);
+        a.gt ? k_fused_ldg<MC, MD, false, true><<<nb, kThreads, 0, s>>>(a)
+             : k_fused_ldg<MC, MD, false, false><<<nb, kThreads, 0, s>>>(a);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return cudaGetLastError();
 }
@@ -983,7 +988,8 @@ cudaError_t fused_md(const FusedArgs& a0, int variant, cudaStream_t s) {
     if (wv < 0) {
         int bps = 0, dev = 0, sms = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &bps, elide ? k_fused_ldg<MC, MD, true> : k_fused_ldg<MC, MD, false>, kThreads, 0);
+            &bps, elide ? k_fused_ldg<MC, MD, true, false> : k_fused_ldg<MC, MD, false, false>,
+            kThreads, 0);
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         // The elided kernel reads only what its flags ask for; every L2
