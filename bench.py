@@ -55,6 +55,15 @@ def bytes_per_px(mc: int, md: int) -> int:
     return (3 + 2 + state + 2 + 2) + (state + 2)
 
 
+def job_pixels(shard: str, W: int, H: int, S: int, world: int) -> int:
+    """Pixels the whole job processes per step (`value` is the aggregate over
+    all ranks): stream shards and row tiles split one fixed job (strong
+    scaling), replicas run one full workload per GPU (weak scaling)."""
+    if shard in ("stream", "rows"):
+        return W * H * S
+    return W * H * S * world
+
+
 def load_peak():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -277,7 +286,7 @@ def main():
     else:  # replica: one independent camera stream per GPU
         my_streams, my_h, seed0, row0 = S, H, 1 + rank, 0
     npx = W * my_h * my_streams
-    total_units = npx * (world if shard == "replica" else 1)
+    total_units = job_pixels(shard, W, H, S, world)
 
     cfg = R.RunConfig.defaults()
     cfg.color_gmm.components = cfg.depth_gmm.components = M
