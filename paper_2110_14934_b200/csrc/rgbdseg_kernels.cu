@@ -983,8 +983,10 @@ cudaError_t fused_ldg_md(const FusedArgs& a, bool elide, cudaStream_t s) {
 template <int MC, int MD>
 cudaError_t fused_md(const FusedArgs& a0, int variant, cudaStream_t s) {
     const bool elide = variant != kLdgDense;
-    static int wave[2] = {-1, -1};  // resident blocks on the device (per variant)
-    int& wv = wave[elide ? 1 : 0];
+    // Resident blocks on the device (per variant), computed once; racing
+    // host threads compute the same value, so a relaxed atomic suffices.
+    static std::atomic<int> wave[2] = {{-1}, {-1}};
+    int wv = wave[elide ? 1 : 0].load(std::memory_order_relaxed);
     if (wv < 0) {
         int bps = 0, dev = 0, sms = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(
@@ -997,6 +999,7 @@ cudaError_t fused_md(const FusedArgs& a0, int variant, cudaStream_t s) {
         // aware planes) measured slower (profiles/variants_r01.json): off.
         wv = elide ? 0 : bps * sms;
         if (const char* e = getenv("RGBDSEG_L2_AHEAD")) wv = atoi(e);  // 0 disables
+        wave[elide ? 1 : 0].store(wv, std::memory_order_relaxed);
     }
     FusedArgs a = a0;
     a.ahead = (unsigned)wv;
