@@ -229,9 +229,11 @@ rgbdseg_fusion* rgbdseg_processor_fusion(rgbdseg_processor* p);
 /* The CUDA stream the processor's kernels run on (cudaStream_t as void*),
  * so callers can time the kernels with events on the launching stream. */
 void* rgbdseg_processor_stream(rgbdseg_processor* p);
-/* Kernel variant: 0 = auto (= 2), 1 = dense write-back of every state word,
- * 2 = write elision (words whose bits did not change are not rewritten).
- * Every variant produces the same bits; they differ only in HBM writes. */
+/* Kernel variant: 0 = auto (= 2), 1 = dense: reads and writes back every
+ * state word, 2 = elided: reads only the components the flag words mark as
+ * touched, runs the step on the warp's touched prefix and rewrites only the
+ * words whose bits changed.  Every variant produces the same bits; they
+ * differ only in HBM traffic and instruction count. */
 int rgbdseg_processor_set_variant(rgbdseg_processor* p, int variant);
 
 /* ---- evaluation: confusion_counts, eval.cpp:11-31 ------------------------
