@@ -451,8 +451,11 @@ def main():
                  if fr[k].dtype == torch.uint16 else fr[k][0].cpu().numpy())
                 for k in ("r", "g", "b", "depth")))
         cb = cpu_reference(sample_frames, W, my_h, M, M, min_seconds=args.cpu_seconds)
+        # SURVEY 8(d) also asks for the single-worker figure (a shorter sample)
+        c1 = cpu_reference(sample_frames, W, my_h, M, M, min_seconds=args.cpu_seconds / 4,
+                           max_seconds=args.cpu_seconds, threads=1)
         cpu = {"value": round(cb["value"], 3), "unit": "Mpix/s", "cores": cb["cores"],
-               "kind": cb["kind"],
+               "kind": cb["kind"], "single_worker_value": round(c1["value"], 3),
                "sample": (f"stream 0 ({W}x{my_h}, seed {seed0}) frames {start}.."
                           f"{start + len(sample_frames) - 1} cycled, {cb['frames']} "
                           f"frames in {cb['seconds']:.1f} s, SequenceProcessor::process "
