@@ -284,17 +284,18 @@ __device__ __forceinline__ void eval_accumulate(bool active, size_t j, size_t st
     const bool uniform = __all_sync(0xffffffffu, !active || s == s0);
     if (uniform) {
         const unsigned g1 = __ballot_sync(0xffffffffu, active && gt);
-        unsigned v = 0u;
-        int slot = 0;
+        // lane 3m+k (k: 0 TP, 1 FP, 2 FN) counts method m's class k
+        const int m = (int)lane / 3, k = (int)lane - 3 * m;
+        unsigned pm = 0u;
 #pragma unroll
-        for (int m = 0; m < NM; ++m) {
-            const unsigned p1 = __ballot_sync(0xffffffffu, active && pred[m]);
-            const unsigned tp = __popc(p1 & g1), fp = __popc(p1 & ~g1), fn = __popc(~p1 & g1);
-            if (lane == 3 * m + 0) { v = tp; slot = m * 4 + 0; }
-            if (lane == 3 * m + 1) { v = fp; slot = m * 4 + 1; }
-            if (lane == 3 * m + 2) { v = fn; slot = m * 4 + 3; }
+        for (int q = 0; q < NM; ++q) {
+            const unsigned p1 = __ballot_sync(0xffffffffu, active && pred[q]);
+            if (q == m) pm = p1;
         }
-        if (lane < 3 * NM && v) atomicAdd(counts + s0 * NM * 4 + slot, (unsigned long long)v);
+        const unsigned sel = k == 0 ? (pm & g1) : (k == 1 ? (pm & ~g1) : (~pm & g1));
+        const unsigned v = __popc(sel);
+        if (m < NM && v)
+            atomicAdd(counts + (s0 * NM + m) * 4 + (k == 2 ? 3 : k), (unsigned long long)v);
     } else if (active) {  // warp across a stream boundary: per-pixel atomics
 #pragma unroll
         for (int m = 0; m < NM; ++m) {
