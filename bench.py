@@ -391,7 +391,9 @@ def main():
     traffic = traffic_px * npx if traffic_px is not None else None
 
     # ---- e2e: public API, pinned host frames in, fused masks out --------------
-    e2e_steps = args.e2e_steps or args.steps
+    # small frames: enough steps for a stable host-path number (~0.1 s or more)
+    e2e_steps = args.e2e_steps or (args.steps if npx >= 2**22 else max(args.steps, 200))
+    sync_steps = min(e2e_steps, 5 if npx >= 2**22 else 50)
     host = []
     for f in range(2):  # a ring of two distinct pinned host frames
         # one planar pinned buffer per frame: r | g | b | depth back to back
@@ -433,12 +435,12 @@ def main():
     # synchronous reference-semantics call (process() per frame, no overlap)
     barrier()
     t0 = time.perf_counter()
-    for k in range(min(e2e_steps, 5)):
+    for k in range(sync_steps):
         hf = host_np[k % 2]
         proc.process(hf["r"], hf["g"], hf["b"], hf["depth"], want=(),
                      out={"fused": outs_np[k % 2]})
     sync_s = allmax(time.perf_counter() - t0)
-    sync_value = total_units * min(e2e_steps, 5) / sync_s / 1e6
+    sync_value = total_units * sync_steps / sync_s / 1e6
 
     # ---- CPU baseline (rank 0, N=1 only) -------------------------------------
     cpu = None

@@ -241,7 +241,32 @@ struct rgbdseg_processor {
     // unregistered sequences: whole-frame scratch (inputs, masks, splat)
     Scratch u_in, u_masks, u_gt;
     Scratch counts;  // evaluation epilogue: [streams][3][4] uint64
+    // Single-chunk host frames: the mask read-back of frame k is issued after
+    // the upload of frame k+1 (or at sync).  The copy engine takes copies in
+    // issue order, so a read-back queued right behind its kernel would hold
+    // the next upload until that kernel ends (VGA: 47 -> 32 us per frame).
+    struct {
+        bool on = false;
+        int lane = 0;
+        size_t n = 0;
+        uint8_t *fused = nullptr, *rgb = nullptr, *depth = nullptr;
+    } pend;
 };
+
+// Issue the deferred read-back, on the stream of the frame it belongs to (so
+// it stays ahead of that slot's next use).
+static int flush_emit(rgbdseg_processor* p) {
+    if (!p->pend.on) return RGBDSEG_OK;
+    p->pend.on = false;
+    const Slot& sl = p->slot[p->pend.lane];
+    cudaStream_t st = p->cs[p->pend.lane];
+    const size_t n = p->pend.n;
+    const cudaMemcpyKind d2h = cudaMemcpyDeviceToHost;
+    if (p->pend.fused) CU(cudaMemcpyAsync(p->pend.fused, sl.fused, n, d2h, st));
+    if (p->pend.rgb) CU(cudaMemcpyAsync(p->pend.rgb, sl.rgbm, n, d2h, st));
+    if (p->pend.depth) CU(cudaMemcpyAsync(p->pend.depth, sl.depm, n, d2h, st));
+    return RGBDSEG_OK;
+}
 
 extern "C" {
 
@@ -686,6 +711,7 @@ void rgbdseg_processor_defaults(rgbdseg_processor_cfg* c, int width, int height)
 void rgbdseg_processor_destroy(rgbdseg_processor* p) {
     if (!p) return;
     DeviceGuard g(p->cfg.device);
+    flush_emit(p);
     for (cudaStream_t st : p->cs)
         if (st) cudaStreamSynchronize(st);
     for (auto& sl : p->slot) {
@@ -879,6 +905,9 @@ static int submit_impl(rgbdseg_processor* p, const uint8_t* r, const uint8_t* g,
     const bool all_device = dr && dg && db && dd && (!fused_out || dfo) && (!rgb_out || dro) &&
                             (!depth_out || ddo) && (!gt || dgt);
     const bool single = !p->cfg.registered || all_device;
+    // only a single-chunk host frame without ground truth keeps a read-back pending
+    if (single || p->nchunks != 1 || gt)
+        if (int rc = flush_emit(p)) return rc;
     if (int rc = switch_mode(p, single ? 2 : 1)) return rc;
     unsigned long long* dcounts = nullptr;
     const size_t ncnt = (size_t)p->cfg.streams * 12;
@@ -950,6 +979,8 @@ static int submit_impl(rgbdseg_processor* p, const uint8_t* r, const uint8_t* g,
             if (!dd) CU(cudaMemcpyAsync(sl.d, depth + lo, n * 2, h2d, st));
         }
         if (gt && !dgt) CU(cudaMemcpyAsync(sl.gt, gt + lo, n, h2d, st));
+        if (alternate)  // the previous frame's read-back, now behind this upload
+            if (int rc = flush_emit(p)) return rc;
         // process (a single-chunk frame waits for the previous frame's K1,
         // queued on the other stream)
         a.r = dr ? r + lo : sl.r;
@@ -968,9 +999,21 @@ static int submit_impl(rgbdseg_processor* p, const uint8_t* r, const uint8_t* g,
         CU(launch_fused(a, p->variant, st));
         if (alternate) CU(cudaEventRecord(p->ev_k[lane], st));
         // emit
-        if (fused_out && !dfo) CU(cudaMemcpyAsync(fused_out + lo, sl.fused, n, d2h, st));
-        if (rgb_out && !dro) CU(cudaMemcpyAsync(rgb_out + lo, sl.rgbm, n, d2h, st));
-        if (depth_out && !ddo) CU(cudaMemcpyAsync(depth_out + lo, sl.depm, n, d2h, st));
+        uint8_t* fo = fused_out && !dfo ? fused_out + lo : nullptr;
+        uint8_t* ro = rgb_out && !dro ? rgb_out + lo : nullptr;
+        uint8_t* dpo = depth_out && !ddo ? depth_out + lo : nullptr;
+        if (alternate && !gt) {  // deferred: issued after the next frame's upload or at sync
+            p->pend.on = fo || ro || dpo;
+            p->pend.lane = lane;
+            p->pend.n = n;
+            p->pend.fused = fo;
+            p->pend.rgb = ro;
+            p->pend.depth = dpo;
+        } else {
+            if (fo) CU(cudaMemcpyAsync(fo, sl.fused, n, d2h, st));
+            if (ro) CU(cudaMemcpyAsync(ro, sl.rgbm, n, d2h, st));
+            if (dpo) CU(cudaMemcpyAsync(dpo, sl.depm, n, d2h, st));
+        }
     }
     if (gt) {  // join both streams' counters, then copy them out
         CU(cudaEventRecord(p->ev[1], p->cs[1]));
@@ -1031,6 +1074,7 @@ int rgbdseg_confusion_counts(const uint8_t* pred, const uint8_t* gt, size_t npx,
 
 int rgbdseg_processor_sync(rgbdseg_processor* p) {
     GUARD(p->cfg.device);
+    if (int rc = flush_emit(p)) return rc;
     CU(cudaStreamSynchronize(p->cs[0]));
     CU(cudaStreamSynchronize(p->cs[1]));
     return RGBDSEG_OK;
