@@ -1154,3 +1154,38 @@ def test_fusion_vector_path_with_partial_chunk(R, port):
         port.lib.orc_fuse(out, cpt, n, 3, r, d)
         assert np.array_equal(got.ravel(), out), step
         assert np.array_equal(fs.cpt.ravel(), cpt), step
+
+
+def test_pipelined_single_chunk_submits_deliver_every_frame(R, cuda):
+    """Single-chunk host frames submitted back to back (read-backs deferred
+    behind the next upload) into distinct pinned buffers, one sync at the
+    end: every frame's fused / rgb / depth masks equal the device path's."""
+    import torch
+
+    S, w, h = 2, 64, 48
+    cfg = R.RunConfig.defaults()
+    a = R.SequenceProcessor(w, h, cfg, streams=S)
+    b = R.SequenceProcessor(w, h, cfg, streams=S)
+    keep, outs, exp = [], [], []
+    for f in range(12):
+        fr = R.render_scenario("A", w, h, 90 + f, streams=S, seed0=6)
+        host = {}
+        for k in ("r", "g", "b", "depth"):
+            v, t = pinned_copy(to_np(fr[k]))
+            host[k] = v
+            keep.append(t)
+        o = {}
+        for k in ("fused", "rgb", "depth_mask"):
+            v, t = pinned_copy(np.zeros((S, h, w), np.uint8))
+            o[k] = v
+            keep.append(t)
+        a.submit(host["r"], host["g"], host["b"], host["depth"], fused=o["fused"], rgb=o["rgb"],
+                 depth_mask=o["depth_mask"])
+        outs.append(o)
+        m = b.process(fr["r"], fr["g"], fr["b"], fr["depth"])
+        exp.append((m.fused.copy(), m.rgb.copy(), m.depth.copy()))
+    a.sync()
+    for f, (o, (ef, er, ed)) in enumerate(zip(outs, exp)):
+        assert np.array_equal(o["fused"], ef), f
+        assert np.array_equal(o["rgb"], er), f
+        assert np.array_equal(o["depth_mask"], ed), f
