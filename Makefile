@@ -19,8 +19,9 @@ lib: $(LIB)
 $(CSRC)/%.o: $(CSRC)/%.cu $(CSRC)/gmm_pixel.cuh $(CSRC)/rgbdseg_kernels.cuh include/rgbdseg_c.h
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
+# cudart is linked shared (libcudart.so.12, the process's one CUDA runtime).
 $(LIB): $(OBJS)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJS)
+	$(NVCC) $(ARCH) -shared -cudart shared -o $@ $(OBJS)
 
 oracle:
 	$(MAKE) -C oracle $(if $(wildcard /root/reference/proj/src),all,$(CURDIR)/oracle/liboracle.so)

@@ -11,6 +11,15 @@
  * device memory of the handle's GPU; the library classifies each pointer with
  * cudaPointerGetAttributes and moves data accordingly.
  *
+ * Stream ordering: the library runs on its own non-blocking CUDA streams,
+ * which are NOT ordered with the legacy default stream.  Device inputs must
+ * be complete before a call reads them: synchronous calls (bank, fusion,
+ * registration, process) need the producer finished; the asynchronous
+ * processor path can instead order itself after a caller's stream with
+ * rgbdseg_processor_wait_stream and publish its results to a caller's stream
+ * with rgbdseg_processor_signal_stream.  Bank and fusion handles borrowed from
+ * a processor drain the processor's queued frames before every call.
+ *
  * Errors: functions return an rgbdseg_status; rgbdseg_last_error() returns a
  * thread-local message for the last failing call on this thread.
  *   RGBDSEG_EINVAL  <-> std::invalid_argument in the reference (bad config,
@@ -229,6 +238,11 @@ rgbdseg_fusion* rgbdseg_processor_fusion(rgbdseg_processor* p);
 /* The CUDA stream the processor's kernels run on (cudaStream_t as void*),
  * so callers can time the kernels with events on the launching stream. */
 void* rgbdseg_processor_stream(rgbdseg_processor* p);
+/* Order the processor's next submits after all work queued so far on
+ * `stream` (cudaStream_t as void*, NULL = legacy default stream), and make
+ * `stream` wait for everything the processor has queued so far. */
+int rgbdseg_processor_wait_stream(rgbdseg_processor* p, void* stream);
+int rgbdseg_processor_signal_stream(rgbdseg_processor* p, void* stream);
 /* Kernel variant: 0 = auto (= 2), 1 = dense: reads and writes back every
  * state word, 2 = elided: reads only the components the flag words mark as
  * touched, runs the step on the warp's touched prefix and rewrites only the

@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("RGBDSEG_B200_LIB", os.path.join(HERE, "librgbdseg_b200.so"))
+# Always the in-tree library built by `make lib` (no environment override).
+LIB_PATH = os.path.join(HERE, "librgbdseg_b200.so")
 
 OK, EINVAL, ECUDA, ENOMEM, ERUNTIME = 0, 1, 2, 3, 4
 COLOR3, DEPTH1, AUGMENTED4 = 0, 1, 2
@@ -133,6 +134,8 @@ SIGNATURES = {
     "rgbdseg_processor_depth_bank": (_vp, [_vp]),
     "rgbdseg_processor_fusion": (_vp, [_vp]),
     "rgbdseg_processor_stream": (_vp, [_vp]),
+    "rgbdseg_processor_wait_stream": (_i, [_vp, _vp]),
+    "rgbdseg_processor_signal_stream": (_i, [_vp, _vp]),
     "rgbdseg_processor_set_variant": (_i, [_vp, _i]),
     "rgbdseg_render_scenario": (_i, [C.c_char, _i, _i, _i, C.c_uint64, _i, _vp, _vp, _vp, _vp,
                                      _vp, _i, _vp]),

@@ -187,6 +187,9 @@ struct rgbdseg_bank {
     cudaStream_t stream = nullptr;
     Scratch s_r, s_g, s_b, s_mask, s_plane;
     float vvar = 0.0f;  // sigma0^2 of the creation cfg: an untouched component's variance
+    // Set when the bank belongs to a processor (rgbdseg_processor_color_bank):
+    // every call on the borrowed handle first drains the processor's streams.
+    rgbdseg_processor* owner = nullptr;
     // Layout view; with a call's cfg it also says whether that call's
     // init_mixture may mark components untouched (same sigma0^2, and the
     // fast step's variance range, gmm_pixel.cuh kVarLo/kVarHi).
@@ -205,6 +208,7 @@ struct rgbdseg_bank {
 struct rgbdseg_fusion {
     size_t npx;
     int limit, device;
+    rgbdseg_processor* owner = nullptr;  // as rgbdseg_bank::owner
     uint8_t* out = nullptr;
     int8_t* cpt = nullptr;
     cudaStream_t stream = nullptr;
@@ -232,6 +236,8 @@ struct rgbdseg_processor {
     cudaStream_t cs[2] = {nullptr, nullptr};
     cudaEvent_t ev[2] = {nullptr, nullptr};  // cross-stream joins (mode switches, counts)
     cudaEvent_t ev_k[2] = {nullptr, nullptr};  // single-chunk frames: K1 of the frame on cs[i]
+    cudaEvent_t ev_user = nullptr;                // rgbdseg_processor_wait_stream
+    cudaEvent_t ev_done[2] = {nullptr, nullptr};  // rgbdseg_processor_signal_stream
     size_t npx = 0, chunk = 0;
     int nchunks = 1;
     Slot slot[2];
@@ -267,6 +273,11 @@ static int flush_emit(rgbdseg_processor* p) {
     if (p->pend.depth) CU(cudaMemcpyAsync(p->pend.depth, sl.depm, n, d2h, st));
     return RGBDSEG_OK;
 }
+
+// A bank / fusion handle borrowed from a processor: finish the processor's
+// queued frames (and its deferred read-back) before the handle's own stream
+// reads or writes the state.
+static int drain_owner(rgbdseg_processor* owner);
 
 extern "C" {
 
@@ -312,6 +323,24 @@ int rgbdseg_step_mixtures(rgbdseg_pixel_mixture* mix, const float* values, int c
     if (channels < 1 || channels > 4)
         return fail(RGBDSEG_EINVAL, "step_pixel: bad observation dimensionality");
     if (n == 0) return RGBDSEG_OK;
+    // Shapes are checked before anything runs, so a rejected call leaves
+    // every record untouched (the kernel's 255 label stays a backstop).
+    {
+        const bool host = !on_device(mix);
+        std::vector<rgbdseg_pixel_mixture> hm;
+        const rgbdseg_pixel_mixture* recs = mix;
+        if (!host) {
+            GUARD(device);
+            hm.resize(n);
+            CU(cudaMemcpy(hm.data(), mix, n * sizeof(PixRec), cudaMemcpyDeviceToHost));
+            recs = hm.data();
+        }
+        for (size_t i = 0; i < n; ++i)
+            if (recs[i].components < 3 || recs[i].components > 5 || recs[i].channels != channels)
+                return fail(RGBDSEG_EINVAL,
+                            "step_pixel: record " + std::to_string(i) +
+                                " has components outside [3,5] or a channel-count mismatch");
+    }
     GUARD(device);
     float* dv;
     PixRec* dr;
@@ -432,11 +461,13 @@ static int bank_xfer(rgbdseg_bank* b, int plane, void* dst, const void* src) {
 
 int rgbdseg_bank_download(const rgbdseg_bank* b, int plane, void* dst) {
     GUARD(b->device);
+    if (int rc = drain_owner(b->owner)) return rc;
     return bank_xfer(const_cast<rgbdseg_bank*>(b), plane, dst, nullptr);
 }
 
 int rgbdseg_bank_upload(rgbdseg_bank* b, int plane, const void* src) {
     GUARD(b->device);
+    if (int rc = drain_owner(b->owner)) return rc;
     return bank_xfer(b, plane, nullptr, src);
 }
 
@@ -465,6 +496,7 @@ int rgbdseg_segment_color(rgbdseg_bank* b, const uint8_t* r, const uint8_t* g, c
                           const rgbdseg_mixture_cfg* cfg, uint8_t* mask_out) {
     if (int rc = bank_call_checks(b, cfg, RGBDSEG_COLOR3, "segment_color")) return rc;
     GUARD(b->device);
+    if (int rc = drain_owner(b->owner)) return rc;
     const void *dr, *dg, *db;
     if (int rc = stage_in(r, b->npx, b->s_r, &dr, b->stream)) return rc;
     if (int rc = stage_in(g, b->npx, b->s_g, &dg, b->stream)) return rc;
@@ -488,6 +520,7 @@ int rgbdseg_segment_depth(rgbdseg_bank* b, const uint16_t* depth_mm,
                           const rgbdseg_mixture_cfg* cfg, uint8_t* mask_out) {
     if (int rc = bank_call_checks(b, cfg, RGBDSEG_DEPTH1, "segment_depth")) return rc;
     GUARD(b->device);
+    if (int rc = drain_owner(b->owner)) return rc;
     const void* dd;
     if (int rc = stage_in(depth_mm, b->npx * 2, b->s_r, &dd, b->stream)) return rc;
     uint8_t* dm = nullptr;
@@ -510,6 +543,7 @@ int rgbdseg_segment_augmented(rgbdseg_bank* b, const uint8_t* r, const uint8_t* 
     if (int rc = bank_call_checks(b, cfg, RGBDSEG_AUGMENTED4, "segment_augmented")) return rc;
     if (!(max_mm > min_mm)) return fail(RGBDSEG_EINVAL, "config: augmented depth range is empty");
     GUARD(b->device);
+    if (int rc = drain_owner(b->owner)) return rc;
     const void *dr, *dg, *db, *dd;
     if (int rc = stage_in(r, b->npx, b->s_r, &dr, b->stream)) return rc;
     if (int rc = stage_in(g, b->npx, b->s_g, &dg, b->stream)) return rc;
@@ -576,6 +610,7 @@ void rgbdseg_fusion_destroy(rgbdseg_fusion* f) {
 int rgbdseg_fusion_step(rgbdseg_fusion* f, const uint8_t* rgb_mask, const uint8_t* depth_mask,
                         uint8_t* out_copy) {
     GUARD(f->device);
+    if (int rc = drain_owner(f->owner)) return rc;
     const void *dr, *dd;
     if (int rc = stage_in(rgb_mask, f->npx, f->s_rgb, &dr, f->stream)) return rc;
     if (int rc = stage_in(depth_mask, f->npx, f->s_dep, &dd, f->stream)) return rc;
@@ -589,6 +624,7 @@ int rgbdseg_fusion_step(rgbdseg_fusion* f, const uint8_t* rgb_mask, const uint8_
 
 int rgbdseg_fusion_download(const rgbdseg_fusion* f, uint8_t* out, int8_t* cpt) {
     GUARD(f->device);
+    if (int rc = drain_owner(f->owner)) return rc;
     CU(cudaStreamSynchronize(f->stream));
     if (out) CU(cudaMemcpy(out, f->out, f->npx, cudaMemcpyDefault));
     if (cpt) CU(cudaMemcpy(cpt, f->cpt, f->npx, cudaMemcpyDefault));
@@ -597,6 +633,7 @@ int rgbdseg_fusion_download(const rgbdseg_fusion* f, uint8_t* out, int8_t* cpt) 
 
 int rgbdseg_fusion_upload(rgbdseg_fusion* f, const uint8_t* out, const int8_t* cpt) {
     GUARD(f->device);
+    if (int rc = drain_owner(f->owner)) return rc;
     CU(cudaStreamSynchronize(f->stream));
     if (out) CU(cudaMemcpy(f->out, out, f->npx, cudaMemcpyDefault));
     if (cpt) CU(cudaMemcpy(f->cpt, cpt, f->npx, cudaMemcpyDefault));
@@ -725,6 +762,9 @@ void rgbdseg_processor_destroy(rgbdseg_processor* p) {
         if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : p->ev_k)
         if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : p->ev_done)
+        if (e) cudaEventDestroy(e);
+    if (p->ev_user) cudaEventDestroy(p->ev_user);
     for (cudaStream_t st : p->cs)
         if (st) cudaStreamDestroy(st);
     rgbdseg_bank_destroy(p->color);
@@ -762,6 +802,8 @@ int rgbdseg_processor_create(const rgbdseg_processor_cfg* cfg, rgbdseg_processor
                                    cfg->fusion_initial_label, cfg->fusion_counter_limit,
                                    cfg->device, &p->fusion);
     if (!rc) {
+        p->color->owner = p->depth->owner = p;
+        p->fusion->owner = p;
         // Large frames: up to 8 chunks of >= 2 Mpx, chunk c on stream c % 2.
         // Smaller frames stay one chunk (per-call CPU cost dominates) and
         // alternate streams frame by frame.  Chunk boundaries fall on
@@ -777,6 +819,9 @@ int rgbdseg_processor_create(const rgbdseg_processor_cfg* cfg, rgbdseg_processor
             if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
         for (cudaEvent_t& ev : p->ev_k)
             if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+        for (cudaEvent_t& ev : p->ev_done)
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_user, cudaEventDisableTiming);
         if (e != cudaSuccess) rc = cuda_fail(e, "processor_create");
     }
     if (rc) {
@@ -841,25 +886,27 @@ static int submit_unregistered(rgbdseg_processor* p, const uint8_t* r, const uin
     const int w = p->cfg.width, h = p->cfg.height, S = p->cfg.streams;
     cudaStream_t st = p->cs[0];
     if (int rc = switch_mode(p, 2)) return rc;
+    // Every staged plane starts on a 256-byte boundary (pitch P), so the
+    // uint16 depth plane is aligned for any pixel count and the byte masks
+    // keep the 16-byte vector kernels.
+    const size_t P = pitch_for(n);
     void* ibuf;
-    if (int rc = p->u_in.get(5 * n, &ibuf)) return rc;
+    if (int rc = p->u_in.get(5 * P, &ibuf)) return rc;
     void* mbuf;
-    if (int rc = p->u_masks.get(5 * n, &mbuf)) return rc;
+    if (int rc = p->u_masks.get(5 * P, &mbuf)) return rc;
     uint8_t* in = static_cast<uint8_t*>(ibuf);
-    uint8_t *rgbm = static_cast<uint8_t*>(mbuf), *depm = rgbm + n, *splat = depm + n,
-            *tmp = splat + n, *reg = tmp + n;
+    uint8_t *rgbm = static_cast<uint8_t*>(mbuf), *depm = rgbm + P, *splat = depm + P,
+            *tmp = splat + P, *reg = tmp + P;
     const uint8_t* src[4] = {r, g, b, reinterpret_cast<const uint8_t*>(depth)};
     const uint8_t* dev[4];
-    size_t off = 0;
     for (int k = 0; k < 4; ++k) {
         const size_t bytes = k == 3 ? 2 * n : n;
         if (on_device(src[k])) {
             dev[k] = src[k];
         } else {
-            CU(cudaMemcpyAsync(in + off, src[k], bytes, cudaMemcpyDefault, st));
-            dev[k] = in + off;
+            CU(cudaMemcpyAsync(in + k * P, src[k], bytes, cudaMemcpyDefault, st));
+            dev[k] = in + k * P;
         }
-        off += bytes;
     }
     FusedArgs a = base_args(p);
     a.fuse = 0;
@@ -1089,6 +1136,25 @@ int rgbdseg_processor_process(rgbdseg_processor* p, const uint8_t* r, const uint
 }
 
 int64_t rgbdseg_processor_frames(const rgbdseg_processor* p) { return p->frames; }
+
+// Stream ordering with a caller's CUDA stream (the library's streams are
+// non-blocking, so they are not ordered with the legacy default stream).
+int rgbdseg_processor_wait_stream(rgbdseg_processor* p, void* stream) {
+    GUARD(p->cfg.device);
+    CU(cudaEventRecord(p->ev_user, (cudaStream_t)stream));
+    CU(cudaStreamWaitEvent(p->cs[0], p->ev_user, 0));
+    CU(cudaStreamWaitEvent(p->cs[1], p->ev_user, 0));
+    return RGBDSEG_OK;
+}
+
+int rgbdseg_processor_signal_stream(rgbdseg_processor* p, void* stream) {
+    GUARD(p->cfg.device);
+    for (int i = 0; i < 2; ++i) {
+        CU(cudaEventRecord(p->ev_done[i], p->cs[i]));
+        CU(cudaStreamWaitEvent((cudaStream_t)stream, p->ev_done[i], 0));
+    }
+    return RGBDSEG_OK;
+}
 rgbdseg_bank* rgbdseg_processor_color_bank(rgbdseg_processor* p) { return p->color; }
 rgbdseg_bank* rgbdseg_processor_depth_bank(rgbdseg_processor* p) { return p->depth; }
 rgbdseg_fusion* rgbdseg_processor_fusion(rgbdseg_processor* p) { return p->fusion; }
@@ -1201,3 +1267,7 @@ int rgbdseg_render_frame(const rgbdseg_scene_frame* f, uint8_t* r, uint8_t* g, u
 }
 
 }  // extern "C"
+
+static int drain_owner(rgbdseg_processor* owner) {
+    return owner ? rgbdseg_processor_sync(owner) : RGBDSEG_OK;
+}

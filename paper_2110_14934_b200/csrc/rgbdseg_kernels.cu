@@ -984,23 +984,31 @@ cudaError_t fused_ldg_md(const FusedArgs& a, bool elide, cudaStream_t s) {
 template <int MC, int MD>
 cudaError_t fused_md(const FusedArgs& a0, int variant, cudaStream_t s) {
     const bool elide = variant != kLdgDense;
-    // Resident blocks on the device (per variant), computed once; racing
-    // host threads compute the same value, so a relaxed atomic suffices.
-    static std::atomic<int> wave[2] = {{-1}, {-1}};
-    int wv = wave[elide ? 1 : 0].load(std::memory_order_relaxed);
-    if (wv < 0) {
-        int bps = 0, dev = 0, sms = 0;
+    // Resident blocks on the launching device (per variant and device
+    // ordinal), computed once; racing host threads compute the same value,
+    // so a relaxed atomic suffices.
+    constexpr int kMaxDev = 64;
+    static std::atomic<int> wave[kMaxDev][2];
+    static std::atomic<bool> wave_init[kMaxDev][2];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int dslot = dev < kMaxDev ? dev : kMaxDev - 1;
+    int wv = wave_init[dslot][elide ? 1 : 0].load(std::memory_order_acquire)
+                 ? wave[dslot][elide ? 1 : 0].load(std::memory_order_relaxed)
+                 : -1;
+    if (wv < 0 || dev >= kMaxDev) {
+        int bps = 0, sms = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(
             &bps, elide ? k_fused_ldg<MC, MD, true, false> : k_fused_ldg<MC, MD, false, false>,
             kThreads, 0);
-        cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         // The elided kernel reads only what its flags ask for; every L2
         // prefetch tried ahead of it (whole tiles, first-round lines, flag-
         // aware planes) measured slower (profiles/variants_r01.json): off.
         wv = elide ? 0 : bps * sms;
         if (const char* e = getenv("RGBDSEG_L2_AHEAD")) wv = atoi(e);  // 0 disables
-        wave[elide ? 1 : 0].store(wv, std::memory_order_relaxed);
+        wave[dslot][elide ? 1 : 0].store(wv, std::memory_order_relaxed);
+        wave_init[dslot][elide ? 1 : 0].store(true, std::memory_order_release);
     }
     FusedArgs a = a0;
     a.ahead = (unsigned)wv;

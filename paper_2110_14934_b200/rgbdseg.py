@@ -56,6 +56,21 @@ def _buf(x, dtype, n: int, what: str, writable=False):
     return x.ctypes.data
 
 
+def _cuda_tensors(*xs):
+    return [x for x in xs if x is not None and _is_torch(x) and x.is_cuda]
+
+
+def _finish_producers(*xs):
+    """Synchronous calls on device tensors: the library's streams are
+    non-blocking (not ordered with torch's stream), so the producing work on
+    the caller's current stream must be complete before the call reads."""
+    ts = _cuda_tensors(*xs)
+    if ts:
+        import torch
+
+        torch.cuda.current_stream(ts[0].device).synchronize()
+
+
 def _as_host(x, dtype, shape):
     """numpy input coerced like pybind11's forcecast (module.cpp:17)."""
     if _is_torch(x):
@@ -307,6 +322,7 @@ class ModelBank:
     def upload_plane(self, pid: int, arr):
         dt = np.uint8 if pid == _lib.FLAGS_PLANE else np.float32
         a = _as_host(arr, dt, self._shape())
+        _finish_producers(a)
         check(lib.rgbdseg_bank_upload(self._h, pid, _buf(a, dt, self.npx, "plane")))
 
     def mean_plane(self, component: int, channel: int) -> np.ndarray:
@@ -366,6 +382,7 @@ def segment_color(bank: ModelBank, r, g, b, cfg: MixtureConfig, workers: int = 1
     r, g, b = (_as_host(x, np.uint8, shp) for x in (r, g, b))
     mask, _ = _mask_out(out, bank.npx, shp)
     c = cfg._c()
+    _finish_producers(r, g, b, mask)
     check(lib.rgbdseg_segment_color(bank._h, _buf(r, np.uint8, bank.npx, "segment_color(r)"),
                                     _buf(g, np.uint8, bank.npx, "segment_color(g)"),
                                     _buf(b, np.uint8, bank.npx, "segment_color(b)"), C.byref(c),
@@ -379,6 +396,7 @@ def segment_depth(bank: ModelBank, depth_mm, cfg: MixtureConfig, workers: int = 
     d = _as_host(depth_mm, np.uint16, shp)
     mask, _ = _mask_out(out, bank.npx, shp)
     c = cfg._c()
+    _finish_producers(d, mask)
     check(lib.rgbdseg_segment_depth(bank._h, _buf(d, np.uint16, bank.npx, "segment_depth"),
                                     C.byref(c), _buf(mask, np.uint8, bank.npx, "mask", True)))
     return mask
@@ -392,6 +410,7 @@ def segment_augmented(bank: ModelBank, r, g, b, depth_mm, rescale: DepthRescale,
     d = _as_host(depth_mm, np.uint16, shp)
     mask, _ = _mask_out(out, bank.npx, shp)
     c = cfg._c()
+    _finish_producers(r, g, b, d, mask)
     check(lib.rgbdseg_segment_augmented(
         bank._h, _buf(r, np.uint8, bank.npx, "segment_augmented(r)"),
         _buf(g, np.uint8, bank.npx, "segment_augmented(g)"),
@@ -437,6 +456,7 @@ class FusionState:
         _check_mask(rgb)
         _check_mask(depth)
         res, _ = _mask_out(out, self.npx, shp)
+        _finish_producers(rgb, depth, res)
         check(lib.rgbdseg_fusion_step(self._h, _buf(rgb, np.uint8, self.npx, "fuse_step(rgb)"),
                                       _buf(depth, np.uint8, self.npx, "fuse_step(depth)"),
                                       _buf(res, np.uint8, self.npx, "out", True)))
@@ -643,6 +663,7 @@ class SequenceProcessor:
             if k not in out:
                 out[k] = np.empty(shp, np.uint8)
         ptrs, keep = self._args(r, g, b, depth, out.get("fused"), out.get("rgb"), out.get("depth"))
+        _finish_producers(*keep, out.get("fused"), out.get("rgb"), out.get("depth"), gt)
         idx = self.frames
         if gt is None:
             check(lib.rgbdseg_processor_process(self._h, *ptrs), "process")
@@ -655,12 +676,23 @@ class SequenceProcessor:
                                                  counts.ctypes.data, *ptrs[4:]), "process")
         return FrameMasks(idx, out.get("rgb"), out.get("depth"), out.get("fused"), counts)
 
-    def submit(self, r, g, b, depth, fused=None, rgb=None, depth_mask=None):
+    def submit(self, r, g, b, depth, fused=None, rgb=None, depth_mask=None, order=True):
         """Enqueue one step without waiting; buffers must stay alive and
-        unmodified until ``sync()``."""
+        unmodified until ``sync()``.  With CUDA tensors and ``order`` the step
+        is queued after the work on torch's current stream, and that stream
+        waits for the step (so torch may consume the outputs directly);
+        ``order=False`` leaves ordering to the caller."""
         ptrs, keep = self._args(r, g, b, depth, fused, rgb, depth_mask)
         self._keep.append((keep, fused, rgb, depth_mask))
+        ts = _cuda_tensors(*keep, fused, rgb, depth_mask) if order else []
+        if ts:
+            import torch
+
+            cur = torch.cuda.current_stream(ts[0].device).cuda_stream
+            check(lib.rgbdseg_processor_wait_stream(self._h, cur), "submit")
         check(lib.rgbdseg_processor_submit(self._h, *ptrs), "submit")
+        if ts:
+            check(lib.rgbdseg_processor_signal_stream(self._h, cur), "submit")
 
     def sync(self):
         check(lib.rgbdseg_processor_sync(self._h), "sync")

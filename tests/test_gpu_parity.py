@@ -544,14 +544,16 @@ def test_dilate_mask_matches_oracle(R, port):
         assert np.array_equal(R.dilate_mask(m, r), exp), r
 
 
-@pytest.mark.parametrize("streams", [1, 3])
-def test_unregistered_processor_matches_oracle(R, port, streams):
+@pytest.mark.parametrize("streams,w,h", [(1, 96, 72), (3, 96, 72), (1, 37, 23), (3, 37, 23)])
+def test_unregistered_processor_matches_oracle(R, port, streams, w, h):
     """processor.cpp:175-179 on the GPU: K1 without fusion, splat, dilation,
-    List 1 -- against the oracle's unregistered processor per stream."""
+    List 1 -- against the oracle's unregistered processor per stream.  37x23
+    (an odd pixel count, host inputs) stages the uint16 depth plane behind
+    three odd-length byte planes: it must land on an aligned pitch."""
     from helpers import random_rig
 
     rng = np.random.default_rng(5)
-    w, h, M = 96, 72, 5
+    M = 5
     a = random_rig(rng, w, h)
     cfg = R.RunConfig.defaults()
     cfg.color_gmm.components = cfg.depth_gmm.components = M
