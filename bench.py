@@ -10,22 +10,37 @@ streams, M=5, batched, sharded by stream across the N GPUs of the box (total
 work fixed -> "scaling": "strong").  Synthetic scenario-A frames (seeds 1..256)
 are rendered on the GPU before timing.  Prints ONE JSON line on rank 0.
 
+Multi-GPU: one process per GPU.  Launched under torchrun (WORLD_SIZE set) it
+must agree with --gpus; started plainly with --gpus N > 1 it re-launches
+itself under torch.distributed.run with N ranks.  NCCL carries only the
+barrier, the max-over-ranks timing and the optional final statistics gather
+(north_star: no data-path collective).  With fewer GPUs than ranks (a 1-GPU
+box), ranks share devices round-robin over gloo and the line says so.
+
 `value` = whole-job Mpix/s with frames resident in HBM (CUDA events on the
 kernel stream, max over ranks); `e2e` = the same metric through the public
-API from pinned host frames with the fused masks read back every step;
-`roofline` = the fused kernel's algorithmic bytes / its event-timed duration
-against MEASURED_PEAKS.json; `cpu_baseline` = the reference compiled from
-source (oracle/_ref) on this host's cores on a bounded sample.
+API from pinned host frames of a progressing sequence with the fused masks
+read back every step; `roofline` = the fused kernel's DRAM bytes (measured in
+this run by an ncu child process, N=1) over its event-timed duration against
+MEASURED_PEAKS.json; `cpu_baseline` = the reference compiled from source
+(oracle/_ref) on this host's cores on a bounded sample.
 """
 from __future__ import annotations
 
 import argparse
+import csv
+import hashlib
+import io
 import json
+import math
 import os
+import shutil
+import socket
 import subprocess
 import sys
 import threading
 import time
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 
@@ -44,7 +59,11 @@ WORKLOADS = {
                "rows"),
 }
 START_FRAME = 95  # timed frames cross scenario A's 1.5x illumination step at 100-112
+LATE_START = 275  # late window: most mixture components touched
+SHADOW_START = 145  # shadow event [150, 180) (synthetic.cpp:250-252)
 L2_BYTES = 126 * 2**20
+METRIC = "RGB-D megapixels/s per GPU & box"
+LIB = os.path.join(ROOT, "paper_2110_14934_b200", "librgbdseg_b200.so")
 
 
 def bytes_per_px(mc: int, md: int) -> int:
@@ -64,6 +83,20 @@ def job_pixels(shard: str, W: int, H: int, S: int, world: int) -> int:
     return W * H * S * world
 
 
+def job_config(name: str, start: int, warmup: int, steps: int, preroll: int, world: int) -> dict:
+    """The `config` object of both arms (identical keys and values, so the
+    driver's same-config check holds)."""
+    text, W, H, S, M, shard = WORKLOADS[name]
+    return {"workload": name, "description": text, "width": W, "height": H, "streams": S,
+            "components_color": M, "components_depth": M, "scenario": "A",
+            "frames": f"{start}..{start + warmup + steps - 1}",
+            "timed_frames": f"{start + warmup}..{start + warmup + steps - 1}",
+            "preroll": (f"frames {start - preroll}..{start - 1} untimed" if preroll
+                        else "none (fresh banks)"),
+            "pixels_per_step": job_pixels(shard, W, H, S, world),
+            "parallelism": f"{shard}-sharded x{world}"}
+
+
 def load_peak():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -78,64 +111,193 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
+def lib_sha() -> str:
+    h = hashlib.sha256()
+    with open(LIB, "rb") as fh:
+        h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
+# ---------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled through NVML every `period_s`
+    during the timed regions (nvidia-smi polls too slowly for a 30 ms
+    region).  The GPU is matched to the CUDA device by UUID."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    NAMES = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+             "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
-    def __init__(self, gpu: int):
-        self.gpu, self.lines, self.proc = gpu, [], None
+    def __init__(self, cuda_index: int, period_s: float = 0.002):
+        self.samples, self.reasons, self.period = [], set(), period_s
+        self.max_mhz, self.h, self._stop, self.t = None, None, threading.Event(), None
+        try:
+            import pynvml as N
+            import torch
+
+            N.nvmlInit()
+            uuid = str(torch.cuda.get_device_properties(cuda_index).uuid)
+            uuid = uuid if uuid.startswith("GPU-") else "GPU-" + uuid
+            try:
+                self.h = N.nvmlDeviceGetHandleByUUID(uuid)
+            except Exception:
+                self.h = N.nvmlDeviceGetHandleByIndex(cuda_index)
+            self.N = N
+            self._reasons = getattr(N, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                N.nvmlDeviceGetCurrentClocksThrottleReasons
+            self.max_mhz = float(N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM))
+        except Exception as e:  # no NVML: the line says so
+            self.err = repr(e)
+
+    def _run(self):
+        N = self.N
+        while not self._stop.is_set():
+            try:
+                self.samples.append(float(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM)))
+                r = self._reasons(self.h)
+                for n, bit in self.NAMES.items():
+                    if r & bit:
+                        self.reasons.add(n)
+            except Exception:
+                pass
+            time.sleep(self.period)
 
     def __enter__(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+        if self.h is not None:
+            self._stop.clear()
+            self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
-        except FileNotFoundError:
-            self.proc = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *a):
-        if self.proc:
-            time.sleep(0.25)
-            self.proc.terminate()
-            self.proc.wait(timeout=5)
+        if self.t:
+            self._stop.set()
+            self.t.join()
+            self.t = None
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[3:7]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0, "source": "nvml " + getattr(self, "err", "no samples")}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "sm_mhz_min": min(self.samples), "reasons": sorted(self.reasons),
+                "samples": len(self.samples), "source": f"nvml every {self.period * 1e3:g} ms"}
+
+
+# ---------------------------------------------------------------- reference arm
+def render_ref_frames(scenes, frames, pool):
+    """Frames of `scenes` rendered by the reference's own render_frame
+    (synthetic.cpp:119-195, oracle/_ref) on a thread pool."""
+    jobs = [(sc, f) for f in frames for sc in scenes]
+    out = list(pool.map(lambda j: j[0].render(j[1]), jobs))
+    n = len(scenes)
+    return [[(fr.r, fr.g, fr.b, fr.depth) for fr in out[k * n:(k + 1) * n]]
+            for k in range(len(frames))]
+
+
+def ref_processors(O, ref, w, h, M, n, threads):
+    """One reference SequenceProcessor per camera stream (the reference has
+    no multi-stream API); streams run concurrently on the host threads, each
+    with workers = threads // streams (at least 1)."""
+    workers = max(1, threads // n)
+    return [O.RefProcessor(ref, w, h, O.color_cfg(M), O.depth_cfg(M), workers=workers)
+            for _ in range(n)], workers
+
+
+def run_frame(pool, procs, frs):
+    list(pool.map(lambda pf: pf[0].process(*pf[1], want_masks=False), zip(procs, frs)))
+
+
+def cpu_sample_shape(W: int, H: int, S: int, threads: int):
+    """A bounded sample of the workload for the CPU: whole 640x480 / 1080p
+    frames of up to max(threads, 4) streams, or a band of rows of a larger
+    frame (<= 4 VGA frames of pixels)."""
+    if W * H > 640 * 480 * 8:
+        return W, min(H, max(1, (640 * 480 * 4) // W)), 1
+    return W, H, min(S, max(4, threads))
+
+
+def run_reference_arm(args):
+    """--impl reference: the reference CPU path (SequenceProcessor::process of
+    the reference compiled from its own sources, oracle/_ref) on this host's
+    cores.  Each step = `fps` frames of the CPU sample; the window continues
+    the same pre-roll as our arm and is sized to >= --ref-seconds timed."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    import oracle as O
+
+    name = args.workload
+    text, W, H, S, M, shard = WORKLOADS[name]
+    threads = os.cpu_count() or 1
+    sw, sh, ss = cpu_sample_shape(W, H, S, threads)
+    start, preroll = args.start, (args.start if args.preroll is None else args.preroll)
+    pool = ThreadPoolExecutor(max_workers=threads)
+    if O.ref_available():
+        ref = O.Ref()
+        kind = "reference"
+        scenes = [O.RefScene(ref, "A", sw, sh, seed=s + 1) for s in range(ss)]
+        procs, workers = ref_processors(O, ref, sw, sh, M, ss, threads)
+        runf = run_frame
+    else:  # the plain-C restatement (pinned to the reference by tests/)
+        port = O.Port()
+        kind, threads, workers = "port", 1, 1
+        scenes = [O.PortScene(port, "A", sw, sh, seed=s + 1) for s in range(ss)]
+        procs = [O.PortProcessor(port, sw * sh, O.color_cfg(M), O.depth_cfg(M))
+                 for _ in range(ss)]
+
+        def runf(_pool, ps, frs):
+            for p, fr in zip(ps, frs):
+                p.process(*fr)
+    # pre-roll (untimed), rendered in batches so host memory stays bounded
+    for f0 in range(start - preroll, start, 8):
+        fl = list(range(f0, min(f0 + 8, start)))
+        for frs in render_ref_frames(scenes, fl, pool):
+            runf(pool, procs, frs)
+    # warm-up frames (untimed) also size the window: fps frames per step so
+    # the K timed steps take >= ref_seconds
+    warm = render_ref_frames(scenes, list(range(start, start + args.warmup)), pool)
+    t_frame = None
+    for k, frs in enumerate(warm):
+        t0 = time.perf_counter()
+        runf(pool, procs, frs)
+        if k >= 1:
+            dt = time.perf_counter() - t0
+            t_frame = dt if t_frame is None else min(t_frame, dt)
+    fps = max(1, math.ceil(1.1 * args.ref_seconds / (args.steps * max(t_frame, 1e-4))))
+    f0 = start + args.warmup
+    frames = render_ref_frames(scenes, list(range(f0, f0 + args.steps * fps)), pool)
+    t0 = time.perf_counter()
+    for frs in frames:
+        runf(pool, procs, frs)
+    dt = time.perf_counter() - t0
+    px = sw * sh * ss * fps * args.steps
+    v = px / dt / 1e6
+    last = start + args.warmup + args.steps * fps - 1
+    sample = (f"{ss} stream(s) of {sw}x{sh} scenario A (seeds 1..{ss}), pre-roll frames "
+              f"{start - preroll}..{start - 1}, warm-up {start}..{start + args.warmup - 1}, timed "
+              f"{start + args.warmup}..{last} ({fps} frame(s) per step, {dt:.1f} s), "
+              f"SequenceProcessor::process fused, one processor per stream, {ss} stream(s) "
+              f"concurrent x workers={workers}")
+    cfg = job_config(name, start, args.warmup, args.steps, preroll, world)
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "Mpix/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "strong" if shard in ("stream", "rows") else "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic", "config": cfg,
+        "cpu_baseline": {"value": round(v, 3), "unit": "Mpix/s", "cores": threads, "kind": kind,
+                         "sample": sample, "timed_seconds": round(dt, 2)},
+        "e2e": {"value": round(v, 3), "unit": "Mpix/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }), flush=True)
+    return 0
 
 
 def cpu_reference(frames_host, width, height, mc, md, min_seconds=10.0, max_seconds=30.0,
                   threads=None):
-    """Time the reference's own SequenceProcessor::process (compiled from
-    /root/reference sources into oracle/_ref) on host frames; falls back to
-    the C restatement if the reference build is absent."""
+    """`cpu_baseline` of our arm: the reference's SequenceProcessor::process
+    (oracle/_ref) on one stream's host frames, workers = all host threads;
+    falls back to the C restatement if the reference build is absent."""
     import oracle as O
 
     threads = threads or os.cpu_count() or 1
@@ -165,64 +327,182 @@ def cpu_reference(frames_host, width, height, mc, md, min_seconds=10.0, max_seco
             "frames": n, "seconds": dt}
 
 
-def run_reference_arm(args):
-    """--impl reference: the reference CPU path on this host's cores, rank 0."""
-    rank, world, _ = dist_env()
-    if rank != 0:
-        return
-    name = args.workload
-    text, W, H, S, M, shard = WORKLOADS[name]
-    import oracle as O
+# ---------------------------------------------------------------- launcher
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
 
-    # Each step: the next frame of `ref_streams` streams (a bounded sample of
-    # the workload), frames rendered by the oracle's C renderer (identical to
-    # the reference's render_frame) before timing.
-    ref_streams = min(S, args.ref_streams)
-    if W * H > 640 * 480 * 4:
-        ref_w, ref_h = W, min(H, max(1, (640 * 480 * 4) // W))  # a row band of the big frame
-    else:
-        ref_w, ref_h = W, H
-    port = O.Port()
-    scenes = [O.PortScene(port, "A", ref_w, ref_h, seed=s + 1) for s in range(ref_streams)]
-    nframes = args.warmup + args.steps
-    frames = [[(lambda fr: (fr.r, fr.g, fr.b, fr.depth))(sc.render(START_FRAME + f))
-               for sc in scenes] for f in range(nframes)]
-    threads = os.cpu_count() or 1
-    if O.ref_available():
-        ref = O.Ref()
-        procs = [O.RefProcessor(ref, ref_w, ref_h, O.color_cfg(M), O.depth_cfg(M),
-                                workers=threads) for _ in scenes]
-        kind = "reference"
-    else:
-        procs = [O.PortProcessor(port, ref_w * ref_h, O.color_cfg(M), O.depth_cfg(M))
-                 for _ in scenes]
-        kind, threads = "port", 1
-    for f in range(args.warmup):
-        for p, fr in zip(procs, frames[f]):
-            p.process(*fr)
-    t0 = time.perf_counter()
-    for f in range(args.warmup, nframes):
-        for p, fr in zip(procs, frames[f]):
-            p.process(*fr)
-    dt = time.perf_counter() - t0
-    px = ref_w * ref_h * ref_streams * args.steps
-    v = px / dt / 1e6
-    sample = (f"{ref_streams} stream(s) of {ref_w}x{ref_h} scenario A, frames "
-              f"{START_FRAME}..{START_FRAME + nframes - 1} ({args.warmup} warm-up), "
-              f"SequenceProcessor::process fused, workers={threads}")
-    print(json.dumps({
-        "impl": "reference", "metric": "RGB-D megapixels/s per GPU & box", "value": round(v, 3),
-        "unit": "Mpix/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
-        "scaling": "strong" if shard in ("stream", "rows") else "weak", "vs_baseline": None,
-        "dtype": "f32", "data": "synthetic",
-        "config": {"workload": name, "description": text, "width": W, "height": H, "streams": S,
-                   "components": M},
-        "cpu_baseline": {"value": round(v, 3), "unit": "Mpix/s", "cores": threads, "kind": kind,
-                         "sample": sample},
-        "e2e": {"value": round(v, 3), "unit": "Mpix/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
-    }), flush=True)
+
+def relaunch(n: int) -> int:
+    """`python bench.py --gpus N` without torchrun: N ranks under
+    torch.distributed.run on this node (rank 0 prints the line)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+           os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+# ---------------------------------------------------------------- traffic (ncu)
+def ncu_bin():
+    return shutil.which("ncu") or ("/usr/local/cuda/bin/ncu"
+                                   if os.path.exists("/usr/local/cuda/bin/ncu") else None)
+
+
+def parse_ncu_csv(text: str):
+    """Per-launch {metric: value in base units} from an ncu --csv launch list."""
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9, "nsecond": 1e-9,
+             "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3}
+    rows = [r for r in csv.reader(io.StringIO(text))]
+    hi = next(i for i, r in enumerate(rows) if "Metric Name" in r)
+    h = rows[hi]
+    ni, vi, ui, idi = (h.index(k) for k in ("Metric Name", "Metric Value", "Metric Unit", "ID"))
+    out = {}
+    for r in rows[hi + 1:]:
+        if len(r) > vi:
+            out.setdefault(r[idi], {})[r[ni]] = float(r[vi].replace(",", "")) * scale[r[ui]]
+    return list(out.values())
+
+
+def measure_traffic(args, npx: int):
+    """DRAM bytes per pixel of this run's K1 launches: the same window
+    re-run in a child process under ncu (dram__bytes_{read,write}.sum of the
+    K timed launches; the child's timings are discarded).  None if ncu is
+    unavailable or fails."""
+    ncu = ncu_bin()
+    if not ncu:
+        return None, "ncu not found"
+    log = os.path.join(ROOT, "gpurun_out", f"traffic_{os.getpid()}.csv")
+    os.makedirs(os.path.dirname(log), exist_ok=True)
+    skip = args.preroll + args.warmup  # one K1 launch per device-resident frame
+    child = [sys.executable, os.path.abspath(__file__), "--child", "traffic", "--workload",
+             args.workload, "--variant", args.variant, "--steps", str(args.steps), "--warmup",
+             str(args.warmup), "--start", str(args.start), "--preroll", str(args.preroll)]
+    cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
+           "--clock-control", "none", "-k", "regex:k_fused", "-s", str(skip), "-c",
+           str(args.steps), "--csv", "--log-file", log, *child]
+    try:
+        r = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True,
+                           timeout=args.traffic_timeout)
+        ls = parse_ncu_csv(open(log).read())
+        if r.returncode != 0 or len(ls) != args.steps:
+            return None, f"ncu rc={r.returncode}, {len(ls)} launches: {r.stdout[-300:]!r}"
+    except Exception as e:  # noqa: BLE001
+        return None, f"ncu failed: {e!r}"
+    finally:
+        if os.path.exists(log):
+            os.remove(log)
+    rd = sum(x["dram__bytes_read.sum"] for x in ls) / len(ls) / npx
+    wr = sum(x["dram__bytes_write.sum"] for x in ls) / len(ls) / npx
+    ms = sum(x["gpu__time_duration.sum"] for x in ls) / len(ls) * 1e3
+    return {"read_bytes_per_px": round(rd, 2), "write_bytes_per_px": round(wr, 2),
+            "bytes_per_px": round(rd + wr, 2), "launches": len(ls), "ncu_ms": round(ms, 4)}, "ok"
+
+
+def stamped_traffic(name: str, variant: str):
+    """profiles/traffic.json entry for this workload, only if it was measured
+    on this exact library build (sha256 prefix of librgbdseg_b200.so)."""
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(tp):
+        return None, "no profiles/traffic.json"
+    doc = json.load(open(tp))
+    key = f"{name}:{'ldg' if variant == 'ldg' else 'auto'}"
+    rec = doc.get("per_px", {}).get(key)
+    if not rec:
+        return None, f"no {key} entry"
+    if doc.get("lib_sha256_16") != lib_sha():
+        return None, "stale: measured on another library build"
+    return rec, "profiles/traffic.json (same library build)"
+
+
+# ---------------------------------------------------------------- our arm
+class Shard:
+    """This rank's share of the workload (stream block, row tile or replica)."""
+
+    def __init__(self, name, rank, world):
+        from paper_2110_14934_b200.shard import row_shard, stream_shard
+
+        self.text, self.W, self.H, self.S, self.M, self.kind = WORKLOADS[name]
+        if self.kind == "stream":
+            s0, s1 = stream_shard(self.S, rank, world)
+            self.streams, self.h, self.seed0, self.row0 = s1 - s0, self.H, 1 + s0, 0
+        elif self.kind == "rows":
+            y0, y1 = row_shard(self.H, rank, world)
+            self.streams, self.h, self.seed0, self.row0 = 1, y1 - y0, 1, y0
+        else:  # replica: one independent camera stream per GPU
+            self.streams, self.h, self.seed0, self.row0 = self.S, self.H, 1 + rank, 0
+        self.npx = self.W * self.h * self.streams
+
+    def render(self, R, frame, device, gt=False):
+        if self.kind == "rows":  # the full-width frame's row band
+            full = R.render_scenario("A", self.W, self.H, frame, streams=1, seed0=self.seed0,
+                                     device=device, with_gt=gt)
+            out = {k: v[:, self.row0:self.row0 + self.h].contiguous() for k, v in full.items()}
+            del full
+            return out
+        return R.render_scenario("A", self.W, self.H, frame, streams=self.streams,
+                                 seed0=self.seed0, device=device, with_gt=gt)
+
+
+def make_proc(R, sh, device, variant):
+    cfg = R.RunConfig.defaults()
+    cfg.color_gmm.components = cfg.depth_gmm.components = sh.M
+    return R.SequenceProcessor(sh.W, sh.h, cfg, streams=sh.streams, device=device,
+                               variant=variant)
+
+
+def preroll(R, proc, sh, frames, device):
+    import torch
+
+    for f in frames:
+        fr = sh.render(R, f, device)
+        torch.cuda.current_stream(device).synchronize()
+        proc.submit(fr["r"], fr["g"], fr["b"], fr["depth"], order=False)
+        proc.sync()
+        del fr
+
+
+def timed_window(R, proc, frames, warmup, steps, ext, flush, clk=None):
+    """W untimed then K timed device-resident steps; per-step CUDA events on
+    the processor's stream.  With `flush`, L2 is flushed before every step by
+    writing a 4x-L2 buffer and then reading another one (the read evicts the
+    dirty lines, so their write-back is not charged to the next step)."""
+    import torch
+
+    for f in range(warmup):
+        fr = frames[f]
+        proc.submit(fr["r"], fr["g"], fr["b"], fr["depth"], order=False)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    region = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    proc.sync()
+    launches0 = R.launch_count()
+    ctx = clk if clk is not None else _Null()
+    with ctx:
+        region[0].record(ext)
+        for k in range(steps):
+            if flush is not None:
+                with torch.cuda.stream(ext):
+                    flush[0].fill_(k & 0xFF)
+                    torch.amax(flush[1], dim=0, out=flush[2])
+            starts[k].record(ext)
+            fr = frames[warmup + k]
+            proc.submit(fr["r"], fr["g"], fr["b"], fr["depth"], order=False)
+            ends[k].record(ext)
+        region[1].record(ext)
+        proc.sync()
+    kernel_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    region_ms = region[0].elapsed_time(region[1])
+    busy = sum(kernel_ms) if flush is not None else region_ms
+    return {"busy_ms": busy, "kernel_ms": kernel_ms, "launches": R.launch_count() - launches0}
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
 
 
 def main():
@@ -232,9 +512,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="streams256", choices=sorted(WORKLOADS))
-    ap.add_argument("--variant", default="auto",
-                    choices=["auto", "ldg", "ldg_elide"])
-    ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps")
+    ap.add_argument("--variant", default="auto", choices=["auto", "ldg", "ldg_elide"])
+    ap.add_argument("--e2e-steps", type=int, default=0, help="0 = auto (host ring <= 4 GB)")
     ap.add_argument("--start", type=int, default=START_FRAME,
                     help="first warm-up frame of scenario A (timed frames follow the warm-up)")
     ap.add_argument("--preroll", type=int, default=None,
@@ -242,25 +521,57 @@ def main():
                          "a bank in mid-sequence state (default: the whole sequence from 0)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    ap.add_argument("--ref-streams", type=int, default=4)
+    ap.add_argument("--ref-seconds", type=float, default=10.0,
+                    help="--impl reference: minimum timed seconds (sets frames per step)")
+    ap.add_argument("--traffic", default="auto", choices=["auto", "ncu", "table", "off"],
+                    help="roofline traffic: ncu child run in this job (N=1), else the stamped "
+                         "table if it matches this library build")
+    ap.add_argument("--traffic-timeout", type=float, default=600.0)
+    ap.add_argument("--windows", default="late,dense,shadow",
+                    help="extra timed windows reported beside the headline ('' = none)")
+    ap.add_argument("--child", default=None, help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
+    if args.preroll is None:
+        args.preroll = args.start
     if args.impl == "reference":
         return run_reference_arm(args)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return relaunch(args.gpus)
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        print(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+        return 2
 
     import torch
 
     import paper_2110_14934_b200 as R
-    from paper_2110_14934_b200.shard import row_shard, stream_shard
 
-    rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    ndev = torch.cuda.device_count()
+    if ndev == 0:
+        print("bench.py: no CUDA device", file=sys.stderr)
+        return 2
+    device = local % ndev
+    oversub = world > ndev
+    torch.cuda.set_device(device)
+    dev = torch.device("cuda", device)
+    comm = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        backend = "gloo" if oversub else "nccl"
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
+        t = torch.ones(1, device=dev if backend == "nccl" else "cpu")
+        dist.all_reduce(t)
+        comm = {"backend": backend, "nranks": dist.get_world_size(),
+                "allreduce_ones": int(t.item()), "devices_visible": ndev,
+                "oversubscribed": oversub}
+        print(f"[rank {rank}] {backend} communicator nranks={dist.get_world_size()} "
+              f"all_reduce(1)={int(t.item())} device=cuda:{device}", file=sys.stderr)
 
     def barrier():
         if world > 1:
@@ -270,244 +581,257 @@ def main():
     def allmax(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=dev if comm["backend"] == "nccl"
+                         else "cpu")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return float(t.item())
 
     name = args.workload
-    text, W, H, S, M, shard = WORKLOADS[name]
-    # ---- this rank's shard -------------------------------------------------
-    if shard == "stream":
-        s0, s1 = stream_shard(S, rank, world)
-        my_streams, my_h, seed0, row0 = s1 - s0, H, 1 + s0, 0
-    elif shard == "rows":
-        y0, y1 = row_shard(H, rank, world)
-        my_streams, my_h, seed0, row0 = 1, y1 - y0, 1, y0
-    else:  # replica: one independent camera stream per GPU
-        my_streams, my_h, seed0, row0 = S, H, 1 + rank, 0
-    npx = W * my_h * my_streams
-    total_units = job_pixels(shard, W, H, S, world)
+    sh = Shard(name, rank, world)
+    npx = sh.npx
+    total_units = job_pixels(sh.kind, sh.W, sh.H, sh.S, world)
+    start, W_, K = args.start, args.warmup, args.steps
+    state_bytes = npx * (bytes_per_px(sh.M, sh.M) - 5)
+    need_flush = state_bytes < 2 * L2_BYTES  # small working sets: flush L2 between steps
+    flush = None
+    if need_flush:
+        flush = (torch.empty(4 * L2_BYTES, dtype=torch.uint8, device=dev),
+                 torch.empty((64, 4 * L2_BYTES // 64 // 4), dtype=torch.int32, device=dev),
+                 torch.empty(4 * L2_BYTES // 64 // 4, dtype=torch.int32, device=dev))
+        flush[1].zero_()
 
-    cfg = R.RunConfig.defaults()
-    cfg.color_gmm.components = cfg.depth_gmm.components = M
-    proc = R.SequenceProcessor(W, my_h, cfg, streams=my_streams, device=local,
-                               variant=args.variant)
+    # ---- A: the headline window, frames resident in HBM ----------------------
+    proc = make_proc(R, sh, device, args.variant)
     ext = torch.cuda.ExternalStream(proc.stream_handle, device=dev)
-
-    start = args.start
-    if args.preroll is None:
-        args.preroll = start
-    # ---- inputs resident in HBM before timing --------------------------------
-    nframes = args.warmup + args.steps
-    frames = []
-    for f in range(nframes):
-        if shard == "rows":  # render the full-width frame's row band: render then slice
-            full = R.render_scenario("A", W, H, start + f, streams=1, seed0=seed0,
-                                     device=local)
-            frames.append({k: v[:, row0:row0 + my_h].contiguous() for k, v in full.items()})
-            del full
-        else:
-            frames.append(R.render_scenario("A", W, H, start + f, streams=my_streams,
-                                            seed0=seed0, device=local))
+    preroll(R, proc, sh, range(start - args.preroll, start), device)
+    frames = [sh.render(R, start + f, device) for f in range(W_ + K)]
     torch.cuda.synchronize()
-    state_bytes = npx * (bytes_per_px(M, M) - 5)
-    flush = state_bytes < 2 * L2_BYTES  # small working sets: flush L2 between steps
-    flush_buf = torch.empty(4 * L2_BYTES, dtype=torch.uint8, device=dev) if flush else None
-
-    def step(f):
-        fr = frames[f]
-        proc.submit(fr["r"], fr["g"], fr["b"], fr["depth"])
-
-    # ---- pre-roll: the sequence's earlier frames, rendered one at a time ------
-    for f in range(start - args.preroll, start):
-        if shard == "rows":
-            full = R.render_scenario("A", W, H, f, streams=1, seed0=seed0, device=local)
-            fr = {k: v[:, row0:row0 + my_h].contiguous() for k, v in full.items()}
-            del full
-        else:
-            fr = R.render_scenario("A", W, H, f, streams=my_streams, seed0=seed0, device=local)
-        torch.cuda.current_stream(dev).synchronize()
-        proc.submit(fr["r"], fr["g"], fr["b"], fr["depth"])
-        proc.sync()
-        del fr
-    for f in range(args.warmup):
-        step(f)
-    # ---- timed region: kernel-only, frames in HBM ----------------------------
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    clk = ClockSampler(device)
     barrier()
-    launches0 = R.launch_count()
-    with ClockSampler(local) as clk:
-        region0 = torch.cuda.Event(enable_timing=True)
-        region1 = torch.cuda.Event(enable_timing=True)
-        region0.record(ext)
-        for k in range(args.steps):
-            if flush:
-                with torch.cuda.stream(ext):
-                    flush_buf.fill_(k & 0xFF)
-            starts[k].record(ext)
-            step(args.warmup + k)
-            ends[k].record(ext)
-        region1.record(ext)
-        proc.sync()
+    win = timed_window(R, proc, frames, W_, K, ext, flush, clk)
+    barrier()
+    busy_ms = allmax(win["busy_ms"])
+    ms_per_step = busy_ms / K
+    value = total_units * K / (busy_ms / 1e3) / 1e6
+    kernel_ms = win["kernel_ms"]
+    if args.child == "traffic":  # ncu child: only the K1 launches of this window matter
+        return 0
+
+    # ---- extra windows (not the headline) ------------------------------------
+    windows = {}
+    wanted = [w for w in args.windows.split(",") if w]
+
+    def window_value(t):
+        b = allmax(t["busy_ms"])
+        return {"value": round(total_units * K / (b / 1e3) / 1e6, 2),
+                "ms_per_step": round(b / K, 4)}
+
+    if "shadow" in wanted or "late" in wanted:
+        # continue A through the sequence: shadow window [145, 170) crosses the
+        # shadow event [150, 180); late window [275, 300) sees the most
+        # touched components
+        cur = start + W_ + K
+        for wname, w0 in (("shadow", SHADOW_START), ("late", LATE_START)):
+            if wname not in wanted or w0 < cur:
+                continue
+            preroll(R, proc, sh, range(cur, w0), device)
+            for f in range(W_ + K):
+                frames[f] = sh.render(R, w0 + f, device)
+            torch.cuda.synchronize()
+            barrier()
+            t = timed_window(R, proc, frames, W_, K, ext, flush)
+            barrier()
+            windows[wname] = {**window_value(t), "frames": f"{w0 + W_}..{w0 + W_ + K - 1}",
+                              "variant": args.variant}
+            cur = w0 + W_ + K
+    del frames
+    if "dense" in wanted and args.variant != "ldg":
+        # the dense write-back kernel on the headline window (fresh processor)
+        pd = make_proc(R, sh, device, "ldg")
+        extd = torch.cuda.ExternalStream(pd.stream_handle, device=dev)
+        preroll(R, pd, sh, range(start - args.preroll, start), device)
+        fr_d = [sh.render(R, start + f, device) for f in range(W_ + K)]
+        torch.cuda.synchronize()
         barrier()
-    launches = R.launch_count() - launches0
-    kernel_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    region_ms = region0.elapsed_time(region1)
-    busy_ms = sum(kernel_ms) if flush else region_ms
-    busy_ms = allmax(busy_ms)
-    ms_per_step = busy_ms / args.steps
-    value = total_units * args.steps / (busy_ms / 1e3) / 1e6
-
-    # ---- roofline of the fused kernel ----------------------------------------
-    # Dense write-back moves exactly the algorithmic 331 B/px of SURVEY 8(d)
-    # (ncu: 337 B/px incl. the tiled flag sectors).  The default kernel reads
-    # only touched mixture components and writes only changed words, so its
-    # bytes are data dependent: achieved/frac use its ncu-measured DRAM bytes
-    # per pixel for this workload (profiles/traffic.json: the same 20 timed
-    # launches of the default window), and the dense-equivalent rate is
-    # reported beside it, labelled as such.
-    peak, peak_src = load_peak()
-    bpp = bytes_per_px(M, M)
-    launch_ms = float(np.mean(kernel_ms))  # one fused launch per step on this rank
-    dense_gbs = bpp * npx / (launch_ms / 1e3) / 1e9
-    variant_key = "ldg" if args.variant == "ldg" else "auto"
-    traffic_px = None
-    tp = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tp):
-        rec = json.load(open(tp))["per_px"].get(f"{name}:{variant_key}")
-        if rec:
-            traffic_px = rec["bytes_per_px"]
-    if args.variant == "ldg" or traffic_px is None:
-        achieved, basis = dense_gbs, f"algorithmic dense bytes ({bpp} B/px, SURVEY 8d)"
-    else:
-        achieved = traffic_px * npx / (launch_ms / 1e3) / 1e9
-        basis = (f"ncu DRAM bytes of this kernel variant ({traffic_px} B/px, "
-                 f"profiles/traffic.json, frames {START_FRAME + 5}..{START_FRAME + 24} after "
-                 f"pre-roll 0..{START_FRAME - 1}): untouched components are not read, "
-                 "unchanged words not written")
-        if start != START_FRAME or args.preroll != start:
-            basis += " [measured for the default window; this run's window differs]"
-    traffic = traffic_px * npx if traffic_px is not None else None
-
-    # ---- e2e: public API, pinned host frames in, fused masks out --------------
-    # small frames: enough steps for a stable host-path number (~0.1 s or more)
-    e2e_steps = args.e2e_steps or (args.steps if npx >= 2**22 else max(args.steps, 200))
-    sync_steps = min(e2e_steps, 5 if npx >= 2**22 else 50)
-    host = []
-    for f in range(2):  # a ring of two distinct pinned host frames
-        # one planar pinned buffer per frame: r | g | b | depth back to back
-        src = frames[args.warmup + f]
-        buf = torch.empty(5 * npx, dtype=torch.uint8, pin_memory=True)
-        hf = {}
-        for idx, k in enumerate(("r", "g", "b")):
-            view = buf[idx * npx:(idx + 1) * npx].view(src[k].shape)
-            view.copy_(src[k])
-            hf[k] = view
-        dview = buf[3 * npx:].view(torch.int16).view(src["depth"].shape)
-        dview.copy_(src["depth"].view(torch.int16))
-        hf["depth"] = dview.view(torch.uint16)
-        hf["_buf"] = buf
-        host.append(hf)
-    outs = [torch.empty((my_streams, my_h, W), dtype=torch.uint8, pin_memory=True)
-            for _ in range(2)]
+        t = timed_window(R, pd, fr_d, W_, K, extd, flush)
+        barrier()
+        windows["dense"] = {**window_value(t), "frames": f"{start + W_}..{start + W_ + K - 1}",
+                            "variant": "ldg (reads and writes every state word)"}
+        del pd, extd, fr_d
     torch.cuda.synchronize()
 
-    def as_np(t):
-        return t.view(torch.int16).numpy().view(np.uint16) if t.dtype == torch.uint16 \
-            else t.numpy()
-
-    host_np = [{k: as_np(v) for k, v in hf.items() if k != "_buf"} for hf in host]
-    outs_np = [o.numpy() for o in outs]
-    for k in range(2):  # warm the host path
-        hf = host_np[k % 2]
-        proc.submit(hf["r"], hf["g"], hf["b"], hf["depth"], fused=outs_np[k % 2])
-    proc.sync()
+    # ---- e2e: public API, pinned host frames of the sequence in, masks out ---
+    e2e_steps = args.e2e_steps
+    if e2e_steps <= 0:
+        ring_cap = max(2, (4 << 30) // (5 * npx))
+        e2e_steps = min(max(K, 150 if npx < 2**22 else K), ring_cap)
+    sync_steps = min(e2e_steps, 5 if npx >= 2**22 else 50)
+    pe = make_proc(R, sh, device, args.variant)
+    preroll(R, pe, sh, range(start - args.preroll, start), device)
+    nhost = e2e_steps + sync_steps
+    host, keep = [], []
+    for f in range(nhost):  # frames start.. of the sequence, each a planar pinned buffer
+        src = sh.render(R, start + f, device)
+        buf = torch.empty(5 * npx, dtype=torch.uint8, pin_memory=True)
+        for idx, k in enumerate(("r", "g", "b")):
+            buf[idx * npx:(idx + 1) * npx].copy_(src[k].reshape(-1))
+        buf[3 * npx:].view(torch.int16).copy_(src["depth"].view(torch.int16).reshape(-1))
+        a = buf.numpy()
+        host.append((a[:npx], a[npx:2 * npx], a[2 * npx:3 * npx],
+                     a[3 * npx:].view(np.uint16)))
+        keep.append(buf)
+        del src
+    outs = [torch.empty(npx, dtype=torch.uint8, pin_memory=True).numpy() for _ in range(2)]
+    torch.cuda.synchronize()
+    shp = (sh.streams, sh.h, sh.W) if sh.streams > 1 else (sh.h, sh.W)
+    host = [tuple(x.reshape(shp) for x in hf) for hf in host]
+    outs = [o.reshape(shp) for o in outs]
     barrier()
-    t0 = time.perf_counter()
-    for k in range(e2e_steps):
-        hf = host_np[k % 2]
-        proc.submit(hf["r"], hf["g"], hf["b"], hf["depth"], fused=outs_np[k % 2])
-    proc.sync()
+    with ClockSampler(device) as clk_e2e:
+        t0 = time.perf_counter()
+        for k in range(e2e_steps):
+            pe.submit(*host[k], fused=outs[k % 2])
+        pe.sync()
+        e2e_s = time.perf_counter() - t0
     barrier()
-    e2e_s = allmax(time.perf_counter() - t0)
+    e2e_s = allmax(e2e_s)
     e2e_value = total_units * e2e_steps / e2e_s / 1e6
-    # synchronous reference-semantics call (process() per frame, no overlap)
     barrier()
     t0 = time.perf_counter()
     for k in range(sync_steps):
-        hf = host_np[k % 2]
-        proc.process(hf["r"], hf["g"], hf["b"], hf["depth"], want=(),
-                     out={"fused": outs_np[k % 2]})
+        pe.process(*host[e2e_steps + k], want=(), out={"fused": outs[k % 2]})
     sync_s = allmax(time.perf_counter() - t0)
     sync_value = total_units * sync_steps / sync_s / 1e6
+    e2e_frames = f"{start}..{start + e2e_steps - 1}"
+
+    # ---- optional final statistics gather (north_star): one evaluation frame
+    stats = None
+    try:
+        f_eval = start + nhost
+        fr = sh.render(R, f_eval, device, gt=True)
+        torch.cuda.synchronize()
+        fm = pe.process(fr["r"], fr["g"], fr["b"], fr["depth"], want=(), gt=fr["gt"])
+        counts = torch.from_numpy(fm.counts.sum(axis=0))  # [rgb, depth, fused][tp fp tn fn]
+        if world > 1:
+            on = dev if comm["backend"] == "nccl" else "cpu"
+            t = counts.to(on)
+            parts = [torch.empty_like(t) for _ in range(world)]
+            torch.distributed.all_gather(parts, t)
+            tot = torch.stack(parts).sum(0).cpu().numpy()
+        else:
+            tot = counts.numpy()
+        f1 = [R.f1_score(int(c[0]), int(c[1]), int(c[3])) for c in tot]
+        stats = {"frame": f_eval, "collective": (f"{comm['backend']} all_gather" if comm
+                                                 else "none (1 rank)"),
+                 "counts_tp_fp_tn_fn": {m: [int(x) for x in c]
+                                        for m, c in zip(("rgb", "depth", "fused"), tot)},
+                 "f1": {m: round(v, 4) for m, v in zip(("rgb", "depth", "fused"), f1)},
+                 "pixels": int(tot[0].sum())}
+        del fr
+    except Exception as e:  # noqa: BLE001 -- reported, never fatal for the bench
+        stats = {"error": repr(e)}
+    del pe, keep, host
+
+    # ---- roofline of the fused kernel ----------------------------------------
+    peak, peak_src = load_peak()
+    bpp = bytes_per_px(sh.M, sh.M)
+    launch_ms = float(np.mean(kernel_ms))  # one fused launch per step on this rank
+    dense_gbs = bpp * npx / (launch_ms / 1e3) / 1e9
+    tr, tr_src = None, "off"
+    if args.traffic in ("auto", "ncu") and world == 1 and rank == 0:
+        tr, tr_src = measure_traffic(args, npx)
+        tr_src = "ncu child run of this window (dram__bytes_read+write of the K timed " \
+                 "launches, cold caches)" if tr else tr_src
+    if tr is None and args.traffic in ("auto", "table"):
+        tr, why = stamped_traffic(name, args.variant)
+        tr_src = why if tr else f"{tr_src}; table: {why}"
+    if args.variant == "ldg" or tr is None:
+        achieved, basis = dense_gbs, f"algorithmic dense bytes ({bpp} B/px, SURVEY 8d)"
+    else:
+        achieved = tr["bytes_per_px"] * npx / (launch_ms / 1e3) / 1e9
+        basis = (f"measured DRAM bytes of this kernel ({tr['bytes_per_px']} B/px = "
+                 f"{tr['read_bytes_per_px']} read + {tr['write_bytes_per_px']} write): "
+                 "untouched components are not read, unchanged words not written")
+    traffic = round(tr["bytes_per_px"] * npx) if tr else None
 
     # ---- CPU baseline (rank 0, N=1 only) -------------------------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle as O
+
         sample_frames = []
-        for f in range(min(nframes, 8)):
-            fr = frames[f]
-            sample_frames.append(tuple(
-                (fr[k][0].view(torch.int16).cpu().numpy().view(np.uint16)
-                 if fr[k].dtype == torch.uint16 else fr[k][0].cpu().numpy())
-                for k in ("r", "g", "b", "depth")))
-        cb = cpu_reference(sample_frames, W, my_h, M, M, min_seconds=args.cpu_seconds)
-        # SURVEY 8(d) also asks for the single-worker figure (a shorter sample)
-        c1 = cpu_reference(sample_frames, W, my_h, M, M, min_seconds=args.cpu_seconds / 4,
-                           max_seconds=args.cpu_seconds, threads=1)
+        # one stream's frames; for 8192^2 a band of rows rendered band-sized
+        cw, chh, _ = cpu_sample_shape(sh.W, sh.h, 1, 1)
+        sc = (O.RefScene(O.Ref(), "A", cw, chh, seed=sh.seed0) if O.ref_available()
+              else O.PortScene(O.Port(), "A", cw, chh, seed=sh.seed0))
+        for f in range(8):
+            fr = sc.render(start + f)
+            sample_frames.append((fr.r, fr.g, fr.b, fr.depth))
+        cb = cpu_reference(sample_frames, cw, chh, sh.M, sh.M, min_seconds=args.cpu_seconds)
+        c1 = cpu_reference(sample_frames, cw, chh, sh.M, sh.M,
+                           min_seconds=args.cpu_seconds / 4, max_seconds=args.cpu_seconds,
+                           threads=1)
         cpu = {"value": round(cb["value"], 3), "unit": "Mpix/s", "cores": cb["cores"],
                "kind": cb["kind"], "single_worker_value": round(c1["value"], 3),
-               "sample": (f"stream 0 ({W}x{my_h}, seed {seed0}) frames {start}.."
-                          f"{start + len(sample_frames) - 1} cycled, {cb['frames']} "
+               "sample": (f"stream 0 ({cw}x{chh}, seed {sh.seed0}) frames {start}.."
+                          f"{start + 7} cycled after an initialisation frame, {cb['frames']} "
                           f"frames in {cb['seconds']:.1f} s, SequenceProcessor::process "
                           f"(fused), workers={cb['cores']}")}
 
     if rank == 0:
+        cfg = job_config(name, start, W_, K, args.preroll, world)
         line = {
-            "metric": "RGB-D megapixels/s per GPU & box",
+            "metric": METRIC,
             "value": round(value, 2),
             "unit": "Mpix/s",
             "n_gpus": world,
-            "steps": args.steps,
-            "warmup": args.warmup,
+            "steps": K,
+            "warmup": W_,
             "ms_per_step": round(ms_per_step, 4),
             "higher_is_better": True,
-            "scaling": "strong" if shard in ("stream", "rows") else "weak",
+            "scaling": "strong" if sh.kind in ("stream", "rows") else "weak",
             "vs_baseline": None,
             "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": name, "description": text, "width": W, "height": H,
-                       "streams": S, "components_color": M, "components_depth": M,
-                       "scenario": "A", "frames": f"{start}..{start + nframes - 1}",
-                       "preroll": (f"frames {start - args.preroll}..{start - 1} "
-                                   "untimed" if args.preroll else "none (fresh banks)"),
-                       "pixels_per_step": total_units, "variant": args.variant,
-                       "parallelism": f"{shard}-sharded x{world}",
-                       "l2": ("flushed between steps (4x L2 buffer), per-step kernel events summed"
-                              if flush else "working set larger than L2 (no flush)")},
+            "config": cfg,
+            "arm": {"variant": args.variant,
+                    "l2": ("flushed before every step (4x-L2 write, then 4x-L2 read), "
+                           "per-step kernel events summed" if need_flush
+                           else "working set larger than L2 (no flush)"),
+                    "library_sha256_16": lib_sha()},
             "per_gpu_value": round(value / world, 2),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
-                         "traffic": round(traffic) if traffic is not None else None,
-                         "achieved_basis": basis, "peak_source": peak_src,
+                         "traffic": traffic, "achieved_basis": basis,
+                         "traffic_source": tr_src, "traffic_detail": tr,
+                         "peak_source": peak_src,
                          "kernel_ms": round(launch_ms, 4),
-                         "kernel_ms_min_max": [round(min(kernel_ms), 4), round(max(kernel_ms), 4)],
+                         "kernel_ms_min_max": [round(min(kernel_ms), 4),
+                                               round(max(kernel_ms), 4)],
                          "dense_algorithmic_bytes_per_px": bpp,
                          "dense_equivalent_gbs": round(dense_gbs, 1),
                          "x_dense_roofline_ceiling": round(dense_gbs / peak, 4)},
+            "windows": windows,
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_value, 2), "unit": "Mpix/s",
                     "h2d_bytes_per_step": 5 * npx, "d2h_bytes_per_step": npx,
-                    "mode": "submit/sync pipelined, pinned planar host frames (r|g|b|depth)",
-                    "sync_process_value": round(sync_value, 2)},
-            "gpu_launches": int(launches),
+                    "mode": ("submit/sync pipelined, pinned planar host frames (r|g|b|depth) "
+                             f"of frames {e2e_frames} after pre-roll, fused masks read back"),
+                    "sync_process_value": round(sync_value, 2),
+                    "sync_process_frames": f"{start + e2e_steps}..{start + nhost - 1}",
+                    "clocks": clk_e2e.summary()},
+            "stats_gather": stats,
+            "gpu_launches": int(win["launches"]),
             "clocks": clk.summary(),
         }
+        if comm:
+            line["comm"] = comm
         print(json.dumps(line), flush=True)
     if world > 1:
+        torch.distributed.barrier()
         torch.distributed.destroy_process_group()
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

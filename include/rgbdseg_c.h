@@ -153,6 +153,10 @@ void rgbdseg_fusion_destroy(rgbdseg_fusion* fs);
 int rgbdseg_fusion_step(rgbdseg_fusion* fs, const uint8_t* rgb_mask, const uint8_t* depth_mask,
                         uint8_t* out_copy);
 int rgbdseg_fusion_download(const rgbdseg_fusion* fs, uint8_t* out, int8_t* cpt);
+/* FusionState::counter_limit is a plain field the reference reads at every
+ * fuse_step (fusion.cpp:24): set it between steps (no validation, like the
+ * reference's fuse_step). */
+int rgbdseg_fusion_set_counter_limit(rgbdseg_fusion* fs, int counter_limit);
 int rgbdseg_fusion_upload(rgbdseg_fusion* fs, const uint8_t* out, const int8_t* cpt);
 
 /* ---- CameraRig / register_mask / dilate_mask: registration.hpp:10-38 -----

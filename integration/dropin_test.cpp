@@ -52,8 +52,8 @@ int main(int argc, char** argv) {
             ++bad;
         }
     }
-    const bool banks = cpu.color_bank()->state_equals(gpu.color_bank()) &&
-                       cpu.depth_bank()->state_equals(gpu.depth_bank());
+    const bool banks = cpu.color_bank()->state_equals(*gpu.color_bank()) &&
+                       cpu.depth_bank()->state_equals(*gpu.depth_bank());
     std::printf("dropin_test: %d frames %dx%d M=%d %s, mask mismatches %d, banks %s\n", frames,
                 w, h, M, unregistered ? "unregistered" : "registered", bad,
                 banks ? "identical" : "DIFFER");

@@ -115,6 +115,7 @@ SIGNATURES = {
     "rgbdseg_fusion_step": (_i, [_vp, _vp, _vp, _vp]),
     "rgbdseg_fusion_download": (_i, [_vp, _vp, _vp]),
     "rgbdseg_fusion_upload": (_i, [_vp, _vp, _vp]),
+    "rgbdseg_fusion_set_counter_limit": (_i, [_vp, _i]),
     "rgbdseg_camera_rig_identity": (None, [C.POINTER(CameraRigC), C.c_double, C.c_double,
                                             C.c_double, C.c_double]),
     "rgbdseg_camera_rig_validate": (_i, [C.POINTER(CameraRigC)]),

@@ -631,6 +631,14 @@ int rgbdseg_fusion_download(const rgbdseg_fusion* f, uint8_t* out, int8_t* cpt) 
     return RGBDSEG_OK;
 }
 
+int rgbdseg_fusion_set_counter_limit(rgbdseg_fusion* f, int counter_limit) {
+    GUARD(f->device);
+    if (int rc = drain_owner(f->owner)) return rc;
+    CU(cudaStreamSynchronize(f->stream));
+    f->limit = counter_limit;
+    return RGBDSEG_OK;
+}
+
 int rgbdseg_fusion_upload(rgbdseg_fusion* f, const uint8_t* out, const int8_t* cpt) {
     GUARD(f->device);
     if (int rc = drain_owner(f->owner)) return rc;
@@ -870,7 +878,7 @@ static FusedArgs base_args(const rgbdseg_processor* p) {
     a.depth = p->depth->view(p->cfg.depth);
     a.ck = to_k(p->cfg.color, p->color->vvar);
     a.dk = to_k(p->cfg.depth, p->depth->vvar);
-    a.limit = p->cfg.fusion_counter_limit;
+    a.limit = p->fusion->limit;
     a.fuse = 1;
     return a;
 }
@@ -925,7 +933,7 @@ static int submit_unregistered(rgbdseg_processor* p, const uint8_t* r, const uin
     CU(launch_register_splat(depm, a.d, w, h, S, to_dev(p->cfg.rig), w, h, splat, st));
     CU(launch_dilate(splat, tmp, reg, w, h, S, p->cfg.dilation_radius, st));
     uint8_t* fcopy = (fused_out && on_device(fused_out)) ? fused_out : nullptr;
-    CU(launch_fuse(p->fusion->out, p->fusion->cpt, rgbm, reg, fcopy, p->cfg.fusion_counter_limit,
+    CU(launch_fuse(p->fusion->out, p->fusion->cpt, rgbm, reg, fcopy, p->fusion->limit,
                    n, st));
     if (gt) {  // evaluation: the three masks against the ground truth
         const void* dgt;

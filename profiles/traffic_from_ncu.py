@@ -51,6 +51,14 @@ def main(paths):
                                      "bytes_per_px": round(rd + wr, 2),
                                      "ncu_ms": round(ms, 4), "launches": n}
         print(w, v, doc["per_px"][f"{w}:{v}"])
+    # stamp the library build the launches ran on (bench.py refuses a table
+    # measured on another build)
+    import hashlib
+
+    lib = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                       "paper_2110_14934_b200", "librgbdseg_b200.so")
+    if os.path.exists(lib):
+        doc["lib_sha256_16"] = hashlib.sha256(open(lib, "rb").read()).hexdigest()[:16]
     json.dump(doc, open(dst, "w"), indent=1, sort_keys=True)
 
 

@@ -489,6 +489,27 @@ def test_cpp_dropin_matches_reference_sequence_processor(cuda):
         assert "banks identical" in r.stdout
 
 
+def test_cpp_dropin_is_source_compatible_with_run_scenario(cuda):
+    """integration/scenario_test: acceptance.cpp's run_scenario
+    (acceptance.cpp:143-174), compiled verbatim from the reference's text
+    against rgbdseg::SequenceProcessor and against rgbdseg::b200's, gives the
+    same hashes, confusion counts and banks (registered with depth holes +
+    augmented, unregistered with a rig, AoS layout); rgb-only / depth-only /
+    augmented method sets, the free segment_* / fuse_step functions with host
+    edits between steps, and the error messages match the reference."""
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "integration", "_build", "scenario_test")
+    if not os.path.exists(exe):
+        pytest.skip("integration/_build/scenario_test not built (needs /root/reference)")
+    for args in (["40", "160", "120"], ["12", "93", "61"]):
+        r = subprocess.run([exe, *args], capture_output=True, text=True, timeout=900)
+        print(r.stdout)
+        assert r.returncode == 0, r.stdout + r.stderr
+        assert "0 failure(s)" in r.stdout
+
+
 # ------------------------------------------------------------ K2 registration
 
 def _rig_from_array(R, a):
