@@ -100,6 +100,27 @@ int rgbdseg_init_mixtures(const float* values, int channels, size_t n,
 int rgbdseg_step_mixtures(rgbdseg_pixel_mixture* mix, const float* values, int channels,
                           size_t n, const rgbdseg_mixture_cfg* cfg, uint8_t* labels, int device);
 
+/* The three pieces of step_pixel on their own, batched over n records:
+ * match_component (mixture.cpp:74-92) -> matched[n]: the component index,
+ *   or -1 for std::nullopt;
+ * classify (mixture.cpp:133-146) of each record's matched[i] (-1 = nullopt)
+ *   -> labels[n], 1 = Foreground;
+ * update_mixture (mixture.cpp:94-131) with each record's matched[i], in
+ *   place.
+ * Like the reference these use each record's own components / channels and
+ * do not validate cfg; records must have 3..5 components and (match,
+ * update) `channels` channels, matched[i] must be -1 or a component index
+ * (the reference's behaviour is undefined otherwise), else RGBDSEG_EINVAL
+ * before anything changes. */
+int rgbdseg_match_components(const rgbdseg_pixel_mixture* mix, const float* values, int channels,
+                             size_t n, const rgbdseg_mixture_cfg* cfg, int32_t* matched,
+                             int device);
+int rgbdseg_classify_mixtures(const rgbdseg_pixel_mixture* mix, const int32_t* matched, size_t n,
+                              const rgbdseg_mixture_cfg* cfg, uint8_t* labels, int device);
+int rgbdseg_update_mixtures(rgbdseg_pixel_mixture* mix, const float* values, int channels,
+                            size_t n, const int32_t* matched, const rgbdseg_mixture_cfg* cfg,
+                            int device);
+
 /* ---- ModelBank: segmenter.hpp:25-55 ------------------------------------
  * Device-resident bank over `npx` = width*height*streams pixels (streams
  * back to back).  Plane ids follow ModelBank's plane order
@@ -221,6 +242,19 @@ int rgbdseg_processor_submit(rgbdseg_processor* p, const uint8_t* r, const uint8
                              const uint8_t* b, const uint16_t* depth, uint8_t* fused_out,
                              uint8_t* rgb_out, uint8_t* depth_out);
 int rgbdseg_processor_sync(rgbdseg_processor* p);
+/* The same step from an INTERLEAVED colour frame: `rgb` holds 3 bytes per
+ * pixel (npx * 3, streams back to back) in R,G,B order (the layout
+ * aos_to_soa consumes, engine.cpp:39-56) or B,G,R (OpenCV / Kinect
+ * capture order); the kernel deinterleaves it in its first load round, so
+ * no host shuffle precedes the upload.  A host buffer holding the packed
+ * colour plane immediately followed by the depth plane moves in one DMA. */
+enum { RGBDSEG_ORDER_RGB = 0, RGBDSEG_ORDER_BGR = 1 };
+int rgbdseg_processor_submit_interleaved(rgbdseg_processor* p, const uint8_t* rgb, int order,
+                                         const uint16_t* depth, uint8_t* fused_out,
+                                         uint8_t* rgb_out, uint8_t* depth_out);
+int rgbdseg_processor_process_interleaved(rgbdseg_processor* p, const uint8_t* rgb, int order,
+                                          const uint16_t* depth, uint8_t* fused_out,
+                                          uint8_t* rgb_out, uint8_t* depth_out);
 /* The same step plus the evaluation epilogue (confusion_counts,
  * eval.cpp:11-31, fused into the kernel): gt = ground-truth mask planes
  * (npx, {0,1}); counts receives int64 [streams][rgb, depth, fused][tp, fp,
@@ -253,6 +287,17 @@ int rgbdseg_processor_signal_stream(rgbdseg_processor* p, void* stream);
  * words whose bits changed.  Every variant produces the same bits; they
  * differ only in HBM traffic and instruction count. */
 int rgbdseg_processor_set_variant(rgbdseg_processor* p, int variant);
+/* Near-threshold report (north_star's parity accounting).  With rel > 0,
+ * every later step first counts -- on the state before the step, in a
+ * separate read-only kernel -- the colour and the depth pixels whose
+ * observation lies within rel * lambda*sigma of a component's match band
+ * in some channel (| |v_c - mu_ic| - lambda*sigma_i | <= rel*lambda*sigma_i,
+ * mixture.cpp:80-84): the pixels a non-bit-exact build could flip.  Setting
+ * it (rel = 0 turns it off) zeroes the counters; counts returns the colour
+ * and depth totals and the pixel-frames examined since. */
+int rgbdseg_processor_set_near_threshold(rgbdseg_processor* p, float rel);
+int rgbdseg_processor_near_threshold_counts(rgbdseg_processor* p, uint64_t* color,
+                                            uint64_t* depth, uint64_t* pixel_frames);
 
 /* ---- evaluation: confusion_counts, eval.cpp:11-31 ------------------------
  * pred/gt: npx mask bytes ({0,1}, host or device) split into `streams` equal

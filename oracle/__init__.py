@@ -256,6 +256,8 @@ class Ref:
         L.rref_step_pixel.argtypes = [C.POINTER(Mix), _f32p, C.POINTER(Cfg), C.POINTER(C.c_int)]
         L.rref_match_component.argtypes = [C.POINTER(Mix), _f32p, C.POINTER(Cfg),
                                            C.POINTER(C.c_int)]
+        L.rref_update_mixture.argtypes = [C.POINTER(Mix), _f32p, C.c_int, C.POINTER(Cfg)]
+        L.rref_classify.argtypes = [C.POINTER(Mix), C.c_int, C.POINTER(Cfg), C.POINTER(C.c_int)]
         L.rref_bank_create.restype = C.c_void_p
         L.rref_bank_create.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(Cfg)]
         L.rref_bank_destroy.argtypes = [C.c_void_p]
@@ -301,6 +303,21 @@ class Ref:
         m = Mix()
         self.check(self.lib.rref_init_mixture(v, len(v), C.byref(cfg), C.byref(m)))
         return m
+
+    def match_component(self, m: Mix, v, cfg: Cfg) -> int:
+        mt = C.c_int()
+        self.check(self.lib.rref_match_component(C.byref(m), np.ascontiguousarray(v, np.float32),
+                                                 C.byref(cfg), C.byref(mt)))
+        return mt.value
+
+    def update_mixture(self, m: Mix, v, matched: int, cfg: Cfg) -> None:
+        self.check(self.lib.rref_update_mixture(C.byref(m), np.ascontiguousarray(v, np.float32),
+                                                matched, C.byref(cfg)))
+
+    def classify(self, m: Mix, matched: int, cfg: Cfg) -> int:
+        lab = C.c_int()
+        self.check(self.lib.rref_classify(C.byref(m), matched, C.byref(cfg), C.byref(lab)))
+        return lab.value
 
     def step_pixel(self, m: Mix, v, cfg: Cfg) -> int:
         lab = C.c_int()

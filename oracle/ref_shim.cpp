@@ -153,6 +153,23 @@ int rref_match_component(const RefMix* m, const float* v, const RefCfg* c, int* 
     });
 }
 
+int rref_update_mixture(RefMix* m, const float* v, int matched, const RefCfg* c) {
+    return guard([&] {
+        PixelMixture p = to_pm(m);
+        update_mixture(p, std::span<const float>(v, static_cast<size_t>(m->channels)),
+                       matched < 0 ? std::nullopt : std::optional<int>(matched), to_ref(c));
+        from_pm(p, m);
+    });
+}
+
+int rref_classify(const RefMix* m, int matched, const RefCfg* c, int* label) {
+    return guard([&] {
+        const auto l = classify(to_pm(m), matched < 0 ? std::nullopt : std::optional<int>(matched),
+                                to_ref(c));
+        *label = l == PixelLabel::Foreground ? 1 : 0;
+    });
+}
+
 // ---- banks (segmenter.hpp:25-69) ----
 void* rref_bank_create(int w, int h, int mode, const RefCfg* c) {
     try {

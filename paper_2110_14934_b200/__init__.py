@@ -6,6 +6,8 @@ from ._lib import launch_count  # noqa: F401  (fails loudly without the CUDA lib
 from .rgbdseg import (  # noqa: F401
     PIXEL_MIXTURE_DTYPE,
     BankMode,
+    aos_to_soa,
+    soa_to_aos,
     CameraRig,
     DepthRescale,
     FrameMasks,
@@ -16,6 +18,8 @@ from .rgbdseg import (  # noqa: F401
     RunConfig,
     SequenceProcessor,
     builtin_scenario_names,
+    classify,
+    classify_mixtures,
     confusion_counts,
     default_config_json,
     dilate_mask,
@@ -23,6 +27,8 @@ from .rgbdseg import (  # noqa: F401
     fuse_step,
     init_mixture,
     init_mixtures,
+    match_component,
+    match_components,
     register_mask,
     render_scenario,
     reset_state,
@@ -31,6 +37,8 @@ from .rgbdseg import (  # noqa: F401
     segment_augmented,
     step_mixtures,
     step_pixel,
+    update_mixture,
+    update_mixtures,
 )
 
 from . import dataset, synthetic  # noqa: F401,E402

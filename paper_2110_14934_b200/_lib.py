@@ -17,6 +17,7 @@ OK, EINVAL, ECUDA, ENOMEM, ERUNTIME = 0, 1, 2, 3, 4
 COLOR3, DEPTH1, AUGMENTED4 = 0, 1, 2
 FLAGS_PLANE = -1
 VARIANTS = {"auto": 0, "ldg": 1, "ldg_elide": 2}
+ORDER = {"rgb": 0, "bgr": 1}
 
 
 class MixtureCfg(C.Structure):
@@ -100,6 +101,9 @@ SIGNATURES = {
     "rgbdseg_mixture_validate": (_i, [C.POINTER(MixtureCfg)]),
     "rgbdseg_init_mixtures": (_i, [_vp, _i, _sz, C.POINTER(MixtureCfg), _vp, _i]),
     "rgbdseg_step_mixtures": (_i, [_vp, _vp, _i, _sz, C.POINTER(MixtureCfg), _vp, _i]),
+    "rgbdseg_match_components": (_i, [_vp, _vp, _i, _sz, C.POINTER(MixtureCfg), _vp, _i]),
+    "rgbdseg_classify_mixtures": (_i, [_vp, _vp, _sz, C.POINTER(MixtureCfg), _vp, _i]),
+    "rgbdseg_update_mixtures": (_i, [_vp, _vp, _i, _sz, _vp, C.POINTER(MixtureCfg), _i]),
     "rgbdseg_bank_create": (_i, [_i, _i, _i, _i, C.POINTER(MixtureCfg), _i, C.POINTER(_vp)]),
     "rgbdseg_bank_destroy": (None, [_vp]),
     "rgbdseg_bank_planes": (_i, [_vp]),
@@ -127,6 +131,8 @@ SIGNATURES = {
     "rgbdseg_processor_process": (_i, [_vp] * 8),
     "rgbdseg_processor_submit": (_i, [_vp] * 8),
     "rgbdseg_processor_sync": (_i, [_vp]),
+    "rgbdseg_processor_submit_interleaved": (_i, [_vp, _vp, _i, _vp, _vp, _vp, _vp]),
+    "rgbdseg_processor_process_interleaved": (_i, [_vp, _vp, _i, _vp, _vp, _vp, _vp]),
     "rgbdseg_processor_process_eval": (_i, [_vp] * 10),
     "rgbdseg_processor_submit_eval": (_i, [_vp] * 10),
     "rgbdseg_confusion_counts": (_i, [_vp, _vp, _sz, _i, _vp, _i]),
@@ -138,6 +144,8 @@ SIGNATURES = {
     "rgbdseg_processor_wait_stream": (_i, [_vp, _vp]),
     "rgbdseg_processor_signal_stream": (_i, [_vp, _vp]),
     "rgbdseg_processor_set_variant": (_i, [_vp, _i]),
+    "rgbdseg_processor_set_near_threshold": (_i, [_vp, C.c_float]),
+    "rgbdseg_processor_near_threshold_counts": (_i, [_vp, _vp, _vp, _vp]),
     "rgbdseg_render_scenario": (_i, [C.c_char, _i, _i, _i, C.c_uint64, _i, _vp, _vp, _vp, _vp,
                                      _vp, _i, _vp]),
     "rgbdseg_render_frame": (_i, [C.POINTER(SceneFrameC), _vp, _vp, _vp, _vp, _vp, _i, _vp]),

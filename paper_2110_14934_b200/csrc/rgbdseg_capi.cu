@@ -247,6 +247,10 @@ struct rgbdseg_processor {
     // unregistered sequences: whole-frame scratch (inputs, masks, splat)
     Scratch u_in, u_masks, u_gt;
     Scratch counts;  // evaluation epilogue: [streams][3][4] uint64
+    // near-threshold report (rgbdseg_processor_set_near_threshold)
+    float near_rel = 0.0f;
+    Scratch near_counts;  // [colour, depth] uint64
+    uint64_t near_pixel_frames = 0;
     // Single-chunk host frames: the mask read-back of frame k is issued after
     // the upload of frame k+1 (or at sync).  The copy engine takes copies in
     // issue order, so a read-back queued right behind its kernel would hold
@@ -379,6 +383,87 @@ int rgbdseg_step_mixtures(rgbdseg_pixel_mixture* mix, const float* values, int c
         }
     }
     return RGBDSEG_OK;
+}
+
+// match_component / classify / update_mixture (mixture.hpp:45-56) batched on
+// the GPU.  Shapes (and, for classify/update, the matched indices) are
+// validated on the host first, so a rejected call changes nothing.
+static int mix_op(int op, rgbdseg_pixel_mixture* mix, const float* values, int channels,
+                  size_t n, const rgbdseg_mixture_cfg* cfg, int32_t* matched, uint8_t* labels,
+                  int device, const char* who) {
+    if (!cfg) return fail(RGBDSEG_EINVAL, std::string(who) + ": null config");
+    if (n == 0) return RGBDSEG_OK;
+    GUARD(device);
+    std::vector<rgbdseg_pixel_mixture> hm;
+    const rgbdseg_pixel_mixture* recs = mix;
+    if (on_device(mix)) {
+        hm.resize(n);
+        CU(cudaMemcpy(hm.data(), mix, n * sizeof(PixRec), cudaMemcpyDeviceToHost));
+        recs = hm.data();
+    }
+    std::vector<int32_t> hmt;
+    const int32_t* mt = matched;
+    if (op != kOpMatch && on_device(matched)) {
+        hmt.resize(n);
+        CU(cudaMemcpy(hmt.data(), matched, n * 4, cudaMemcpyDeviceToHost));
+        mt = hmt.data();
+    }
+    for (size_t i = 0; i < n; ++i) {
+        const int M = recs[i].components;
+        if (M < 3 || M > 5 || recs[i].channels < 1 || recs[i].channels > 4 ||
+            (op != kOpClassify && recs[i].channels != channels))
+            return fail(RGBDSEG_EINVAL, std::string(who) + ": record " + std::to_string(i) +
+                                            " has components outside [3,5] or a channel-count "
+                                            "mismatch");
+        if (op != kOpMatch && (mt[i] < -1 || mt[i] >= M))
+            return fail(RGBDSEG_EINVAL, std::string(who) + ": record " + std::to_string(i) +
+                                            " matched index out of range");
+    }
+    PixRec* dr = nullptr;
+    float* dv = nullptr;
+    int* dm = nullptr;
+    uint8_t* dl = nullptr;
+    int rc = dalloc(&dr, n);
+    if (!rc && op != kOpClassify) rc = dalloc(&dv, n * channels);
+    if (!rc) rc = dalloc(&dm, n);
+    if (!rc && op == kOpClassify) rc = dalloc(&dl, n);
+    cudaError_t e = cudaSuccess;
+    if (!rc) {
+        e = cudaMemcpy(dr, recs, n * sizeof(PixRec), cudaMemcpyDefault);
+        if (e == cudaSuccess && dv) e = cudaMemcpy(dv, values, n * channels * 4, cudaMemcpyDefault);
+        if (e == cudaSuccess && op != kOpMatch) e = cudaMemcpy(dm, mt, n * 4, cudaMemcpyDefault);
+        if (e == cudaSuccess) e = launch_mix_op(dr, dv, n, to_k(*cfg), op, dm, dl, 0);
+        if (e == cudaSuccess && op == kOpMatch) e = cudaMemcpy(matched, dm, n * 4, cudaMemcpyDefault);
+        if (e == cudaSuccess && op == kOpClassify) e = cudaMemcpy(labels, dl, n, cudaMemcpyDefault);
+        if (e == cudaSuccess && op == kOpUpdate)
+            e = cudaMemcpy(mix, dr, n * sizeof(PixRec), cudaMemcpyDefault);
+        if (e != cudaSuccess) rc = cuda_fail(e, who);
+    }
+    dfree(dr);
+    dfree(dv);
+    dfree(dm);
+    dfree(dl);
+    return rc;
+}
+
+int rgbdseg_match_components(const rgbdseg_pixel_mixture* mix, const float* values, int channels,
+                             size_t n, const rgbdseg_mixture_cfg* cfg, int32_t* matched,
+                             int device) {
+    return mix_op(kOpMatch, const_cast<rgbdseg_pixel_mixture*>(mix), values, channels, n, cfg,
+                  matched, nullptr, device, "match_component");
+}
+
+int rgbdseg_classify_mixtures(const rgbdseg_pixel_mixture* mix, const int32_t* matched, size_t n,
+                              const rgbdseg_mixture_cfg* cfg, uint8_t* labels, int device) {
+    return mix_op(kOpClassify, const_cast<rgbdseg_pixel_mixture*>(mix), nullptr, 0, n, cfg,
+                  const_cast<int32_t*>(matched), labels, device, "classify");
+}
+
+int rgbdseg_update_mixtures(rgbdseg_pixel_mixture* mix, const float* values, int channels,
+                            size_t n, const int32_t* matched, const rgbdseg_mixture_cfg* cfg,
+                            int device) {
+    return mix_op(kOpUpdate, mix, values, channels, n, cfg, const_cast<int32_t*>(matched),
+                  nullptr, device, "update_mixture");
 }
 
 // ------------------------------------------------------------ banks
@@ -872,6 +957,14 @@ static int switch_mode(rgbdseg_processor* p, int mode) {
     return RGBDSEG_OK;
 }
 
+// The near-threshold pass ahead of K1 (same stream, same pixels).
+static int near_pass(rgbdseg_processor* p, const FusedArgs& a, cudaStream_t st) {
+    if (!(p->near_rel > 0.0f)) return RGBDSEG_OK;
+    CU(launch_near(a, p->near_rel, static_cast<unsigned long long*>(p->near_counts.p), st));
+    p->near_pixel_frames += a.n;
+    return RGBDSEG_OK;
+}
+
 static FusedArgs base_args(const rgbdseg_processor* p) {
     FusedArgs a{};
     a.color = p->color->view(p->cfg.color);
@@ -889,7 +982,7 @@ static FusedArgs base_args(const rgbdseg_processor* p) {
 static int submit_unregistered(rgbdseg_processor* p, const uint8_t* r, const uint8_t* g,
                                const uint8_t* b, const uint16_t* depth, uint8_t* fused_out,
                                uint8_t* rgb_out, uint8_t* depth_out, const uint8_t* gt,
-                               unsigned long long* dcounts) {
+                               unsigned long long* dcounts, int pack) {
     const size_t n = p->npx;
     const int w = p->cfg.width, h = p->cfg.height, S = p->cfg.streams;
     cudaStream_t st = p->cs[0];
@@ -906,9 +999,10 @@ static int submit_unregistered(rgbdseg_processor* p, const uint8_t* r, const uin
     uint8_t *rgbm = static_cast<uint8_t*>(mbuf), *depm = rgbm + P, *splat = depm + P,
             *tmp = splat + P, *reg = tmp + P;
     const uint8_t* src[4] = {r, g, b, reinterpret_cast<const uint8_t*>(depth)};
-    const uint8_t* dev[4];
+    const uint8_t* dev[4] = {nullptr, nullptr, nullptr, nullptr};
     for (int k = 0; k < 4; ++k) {
-        const size_t bytes = k == 3 ? 2 * n : n;
+        if (pack && (k == 1 || k == 2)) continue;  // one interleaved plane at k = 0
+        const size_t bytes = k == 3 ? 2 * n : (pack ? 3 * n : n);
         if (on_device(src[k])) {
             dev[k] = src[k];
         } else {
@@ -919,8 +1013,10 @@ static int submit_unregistered(rgbdseg_processor* p, const uint8_t* r, const uin
     FusedArgs a = base_args(p);
     a.fuse = 0;
     a.r = dev[0];
-    a.g = dev[1];
-    a.b = dev[2];
+    a.g = pack ? dev[0] : dev[1];
+    a.b = pack ? dev[0] : dev[2];
+    a.packed = pack != 0;
+    a.bgr = pack == 2;
     a.d = reinterpret_cast<const uint16_t*>(dev[3]);
     a.rgb_mask = rgbm;
     a.depth_mask = depm;
@@ -928,6 +1024,7 @@ static int submit_unregistered(rgbdseg_processor* p, const uint8_t* r, const uin
     a.cpt = p->fusion->cpt;
     a.base = 0;
     a.n = n;
+    if (int rc = near_pass(p, a, st)) return rc;
     CU(launch_fused(a, p->variant, st));
     CU(cudaMemsetAsync(splat, 0, n, st));
     CU(launch_register_splat(depm, a.d, w, h, S, to_dev(p->cfg.rig), w, h, splat, st));
@@ -949,11 +1046,17 @@ static int submit_unregistered(rgbdseg_processor* p, const uint8_t* r, const uin
     return RGBDSEG_OK;
 }
 
+// pack: 0 = planar r, g, b; 1 / 2 = ONE interleaved colour plane `r` of 3
+// bytes per pixel in R,G,B / B,G,R order (g, b ignored), deinterleaved by K1.
 static int submit_impl(rgbdseg_processor* p, const uint8_t* r, const uint8_t* g, const uint8_t* b,
                        const uint16_t* depth, uint8_t* fused_out, uint8_t* rgb_out,
-                       uint8_t* depth_out, const uint8_t* gt, int64_t* counts_out) {
+                       uint8_t* depth_out, const uint8_t* gt, int64_t* counts_out,
+                       int pack = 0) {
+    if (pack) g = b = r;
     if (!r || !g || !b || !depth) return fail(RGBDSEG_EINVAL, "process: null input plane");
     if (gt && !counts_out) return fail(RGBDSEG_EINVAL, "process: ground truth without counts");
+    if (gt && pack)
+        return fail(RGBDSEG_EINVAL, "process: evaluation takes planar colour input");
     const bool dr = on_device(r), dg = on_device(g), db = on_device(b), dd = on_device(depth);
     const bool dfo = on_device(fused_out), dro = on_device(rgb_out), ddo = on_device(depth_out);
     const bool dgt = gt && on_device(gt);
@@ -977,7 +1080,8 @@ static int submit_impl(rgbdseg_processor* p, const uint8_t* r, const uint8_t* g,
         }
     }
     if (!p->cfg.registered) {
-        int rc = submit_unregistered(p, r, g, b, depth, fused_out, rgb_out, depth_out, gt, dcounts);
+        int rc = submit_unregistered(p, r, g, b, depth, fused_out, rgb_out, depth_out, gt, dcounts,
+                                     pack);
         if (!rc && gt)
             CU(cudaMemcpyAsync(counts_out, dcounts, ncnt * 8, cudaMemcpyDefault, p->cs[0]));
         return rc;
@@ -985,6 +1089,8 @@ static int submit_impl(rgbdseg_processor* p, const uint8_t* r, const uint8_t* g,
     FusedArgs a = base_args(p);
     a.counts = dcounts;
     a.stream_px = (size_t)p->cfg.width * p->cfg.height;
+    a.packed = pack != 0;
+    a.bgr = pack == 2;
     if (all_device) {  // device-resident frames: one launch over every pixel
         a.r = r;
         a.g = g;
@@ -998,6 +1104,7 @@ static int submit_impl(rgbdseg_processor* p, const uint8_t* r, const uint8_t* g,
         a.base = 0;
         a.n = p->npx;
         a.gt = gt;
+        if (int rc = near_pass(p, a, p->cs[0])) return rc;
         CU(launch_fused(a, p->variant, p->cs[0]));
         if (gt) {
             CU(launch_counts_tn(dcounts, p->cfg.streams, 3, a.stream_px, p->cs[0]));
@@ -1008,8 +1115,11 @@ static int submit_impl(rgbdseg_processor* p, const uint8_t* r, const uint8_t* g,
     }
     if (int rc = ensure_slots(p)) return rc;
     // planar host frame: the four planes back to back in one host buffer
-    const bool planar = !dr && !dg && !db && !dd && g == r + p->npx && b == g + p->npx &&
-                        reinterpret_cast<const uint8_t*>(depth) == b + p->npx;
+    // (interleaved: the 3-byte plane then depth)
+    const bool planar = !dr && !dg && !db && !dd &&
+                        (pack ? reinterpret_cast<const uint8_t*>(depth) == r + 3 * p->npx
+                              : (g == r + p->npx && b == g + p->npx &&
+                                 reinterpret_cast<const uint8_t*>(depth) == b + p->npx));
     const bool alternate = p->nchunks == 1;
     const cudaMemcpyKind h2d = cudaMemcpyHostToDevice, d2h = cudaMemcpyDeviceToHost;
     for (int c = 0; c < p->nchunks; ++c) {
@@ -1020,7 +1130,14 @@ static int submit_impl(rgbdseg_processor* p, const uint8_t* r, const uint8_t* g,
         Slot& sl = p->slot[lane];
         cudaStream_t st = p->cs[lane];
         // ingest
-        if (planar) {  // r, g, b rows of this chunk in one 2-D copy, depth in one
+        if (pack) {  // the chunk's 3n interleaved bytes into the slot's r|g|b span
+            if (planar && n == p->chunk && n == p->npx) {
+                CU(cudaMemcpyAsync(sl.r, r, 5 * n, h2d, st));
+            } else {
+                if (!dr) CU(cudaMemcpyAsync(sl.r, r + 3 * lo, 3 * n, h2d, st));
+                if (!dd) CU(cudaMemcpyAsync(sl.d, depth + lo, n * 2, h2d, st));
+            }
+        } else if (planar) {  // r, g, b rows of this chunk in one 2-D copy, depth in one
             if (n == p->chunk && n == p->npx) {
                 CU(cudaMemcpyAsync(sl.r, r, 5 * n, h2d, st));
             } else {
@@ -1038,9 +1155,9 @@ static int submit_impl(rgbdseg_processor* p, const uint8_t* r, const uint8_t* g,
             if (int rc = flush_emit(p)) return rc;
         // process (a single-chunk frame waits for the previous frame's K1,
         // queued on the other stream)
-        a.r = dr ? r + lo : sl.r;
-        a.g = dg ? g + lo : sl.g;
-        a.b = db ? b + lo : sl.b;
+        a.r = dr ? r + (pack ? 3 * lo : lo) : sl.r;
+        a.g = pack ? a.r : (dg ? g + lo : sl.g);
+        a.b = pack ? a.r : (db ? b + lo : sl.b);
         a.d = dd ? depth + lo : sl.d;
         a.gt = gt ? (dgt ? gt + lo : sl.gt) : nullptr;
         a.rgb_mask = rgb_out ? (dro ? rgb_out + lo : sl.rgbm) : nullptr;
@@ -1051,6 +1168,7 @@ static int submit_impl(rgbdseg_processor* p, const uint8_t* r, const uint8_t* g,
         a.out = p->fusion->out + lo;
         a.cpt = p->fusion->cpt + lo;
         if (alternate) CU(cudaStreamWaitEvent(st, p->ev_k[lane ^ 1], 0));
+        if (int rc = near_pass(p, a, st)) return rc;
         CU(launch_fused(a, p->variant, st));
         if (alternate) CU(cudaEventRecord(p->ev_k[lane], st));
         // emit
@@ -1086,6 +1204,25 @@ int rgbdseg_processor_submit(rgbdseg_processor* p, const uint8_t* r, const uint8
                              uint8_t* rgb_out, uint8_t* depth_out) {
     GUARD(p->cfg.device);
     return submit_impl(p, r, g, b, depth, fused_out, rgb_out, depth_out, nullptr, nullptr);
+}
+
+int rgbdseg_processor_submit_interleaved(rgbdseg_processor* p, const uint8_t* rgb, int order,
+                                         const uint16_t* depth, uint8_t* fused_out,
+                                         uint8_t* rgb_out, uint8_t* depth_out) {
+    GUARD(p->cfg.device);
+    if (order != RGBDSEG_ORDER_RGB && order != RGBDSEG_ORDER_BGR)
+        return fail(RGBDSEG_EINVAL, "process: unknown channel order");
+    return submit_impl(p, rgb, nullptr, nullptr, depth, fused_out, rgb_out, depth_out, nullptr,
+                       nullptr, order == RGBDSEG_ORDER_BGR ? 2 : 1);
+}
+
+int rgbdseg_processor_process_interleaved(rgbdseg_processor* p, const uint8_t* rgb, int order,
+                                          const uint16_t* depth, uint8_t* fused_out,
+                                          uint8_t* rgb_out, uint8_t* depth_out) {
+    if (int rc = rgbdseg_processor_submit_interleaved(p, rgb, order, depth, fused_out, rgb_out,
+                                                      depth_out))
+        return rc;
+    return rgbdseg_processor_sync(p);
 }
 
 int rgbdseg_processor_submit_eval(rgbdseg_processor* p, const uint8_t* r, const uint8_t* g,
@@ -1167,6 +1304,32 @@ rgbdseg_bank* rgbdseg_processor_color_bank(rgbdseg_processor* p) { return p->col
 rgbdseg_bank* rgbdseg_processor_depth_bank(rgbdseg_processor* p) { return p->depth; }
 rgbdseg_fusion* rgbdseg_processor_fusion(rgbdseg_processor* p) { return p->fusion; }
 void* rgbdseg_processor_stream(rgbdseg_processor* p) { return (void*)p->cs[0]; }
+
+int rgbdseg_processor_set_near_threshold(rgbdseg_processor* p, float rel) {
+    GUARD(p->cfg.device);
+    if (int rc = rgbdseg_processor_sync(p)) return rc;
+    if (!(rel >= 0.0f)) return fail(RGBDSEG_EINVAL, "near-threshold: rel must be >= 0");
+    p->near_rel = rel;
+    if (rel > 0.0f) {
+        void* c;
+        if (int rc = p->near_counts.get(2 * sizeof(unsigned long long), &c)) return rc;
+        CU(cudaMemset(c, 0, 2 * sizeof(unsigned long long)));
+        p->near_pixel_frames = 0;
+    }
+    return RGBDSEG_OK;
+}
+
+int rgbdseg_processor_near_threshold_counts(rgbdseg_processor* p, uint64_t* color,
+                                            uint64_t* depth, uint64_t* pixel_frames) {
+    GUARD(p->cfg.device);
+    if (int rc = rgbdseg_processor_sync(p)) return rc;
+    unsigned long long h[2] = {0, 0};
+    if (p->near_counts.p) CU(cudaMemcpy(h, p->near_counts.p, sizeof h, cudaMemcpyDeviceToHost));
+    if (color) *color = h[0];
+    if (depth) *depth = h[1];
+    if (pixel_frames) *pixel_frames = p->near_pixel_frames;
+    return RGBDSEG_OK;
+}
 
 int rgbdseg_processor_set_variant(rgbdseg_processor* p, int variant) {
     if (variant < kAuto || variant > kLdgElide) return fail(RGBDSEG_EINVAL, "unknown kernel variant");

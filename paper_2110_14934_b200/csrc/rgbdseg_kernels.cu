@@ -442,14 +442,26 @@ __device__ __forceinline__ void fused_core(const FusedArgs& a, size_t i0, unsign
 }
 
 // One pixel of K1 with its first round loaded straight from global memory.
-template <int MC, int MD, bool kElide>
+// kPacked: the colour input is one interleaved 3-byte-per-pixel plane
+// (a.r, RGB or BGR by a.bgr -- engine.cpp:39-56's aos_to_soa layout, or
+// OpenCV's BGR), deinterleaved here in the first load round: a warp's three
+// byte loads cover the same 96 contiguous bytes the three planar loads would.
+template <int MC, int MD, bool kElide, bool kPacked = false>
 __device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i0, unsigned t,
                                             uint32_t (&lab)[3]) {
     const PixAddr<MC, MD> p(a, i0, t);
     Round1 r;
-    r.vc[0] = (float)ld_h<kElide>(a.r + i0 + t);
-    r.vc[1] = (float)ld_h<kElide>(a.g + i0 + t);
-    r.vc[2] = (float)ld_h<kElide>(a.b + i0 + t);
+    if constexpr (kPacked) {
+        const uint8_t* px = a.r + (i0 + t) * 3;
+        const int ro = a.bgr ? 2 : 0;
+        r.vc[0] = (float)ld_h<kElide>(px + ro);
+        r.vc[1] = (float)ld_h<kElide>(px + 1);
+        r.vc[2] = (float)ld_h<kElide>(px + (2 - ro));
+    } else {
+        r.vc[0] = (float)ld_h<kElide>(a.r + i0 + t);
+        r.vc[1] = (float)ld_h<kElide>(a.g + i0 + t);
+        r.vc[2] = (float)ld_h<kElide>(a.b + i0 + t);
+    }
     r.raw = ld_h<kElide>(a.d + i0 + t);
     r.cf = ld_h<kElide>(p.cflag());
     r.df = ld_h<kElide>(p.dflag());
@@ -464,7 +476,7 @@ __device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i0, unsig
 
 // kEval: with the evaluation epilogue (a.gt set).  A separate instantiation,
 // so the plain kernel's register allocation carries none of it (measured 6%).
-template <int MC, int MD, bool kElide, bool kEval>
+template <int MC, int MD, bool kElide, bool kEval, bool kPacked = false>
 __global__ void __launch_bounds__(kThreads, RGBDSEG_FUSED_MIN_BLOCKS(kElide))
     k_fused_ldg(const __grid_constant__ FusedArgs a) {
     const size_t i0 = (size_t)blockIdx.x * kThreads;
@@ -488,11 +500,58 @@ __global__ void __launch_bounds__(kThreads, RGBDSEG_FUSED_MIN_BLOCKS(kElide))
         }
     }
     uint32_t lab[3] = {0u, 0u, 0u};
-    if (active) fused_pixel<MC, MD, kElide>(a, i0, threadIdx.x, lab);
+    if (active) fused_pixel<MC, MD, kElide, kPacked>(a, i0, threadIdx.x, lab);
     if constexpr (kEval) {  // evaluation epilogue: the masks never leave registers
         const uint32_t g = active ? (uint32_t)a.gt[i] : 0u;
         eval_accumulate<3>(active, a.base + i, a.stream_px, lab, g, a.counts);
     }
+}
+
+// ---------------------------------------------------------------- near threshold
+// Diagnostic pass (north_star's parity report): counts the pixels of one
+// bank whose observation lies within `rel` (relative) of some component's
+// match band in some channel, | |v_c - mu_ic| - lambda*sigma_i | <=
+// rel * lambda*sigma_i, on the state BEFORE this frame's step.  Such a
+// pixel is where an FMA-contracted or reassociated build would flip the
+// match test (mixture.cpp:80-84).  Read-only; launched before K1 on the
+// same stream when the processor's report is on.
+template <int M, int C>
+__global__ void __launch_bounds__(kThreads)
+    k_near(BankView bk, const uint8_t* __restrict__ r, const uint8_t* __restrict__ g,
+           const uint8_t* __restrict__ b, const uint16_t* __restrict__ d, size_t base, size_t n,
+           float lambda, float rel, unsigned long long* count) {
+    const size_t i = (size_t)blockIdx.x * kThreads + threadIdx.x;
+    bool near = false;
+    if (i < n) {
+        const size_t j = base + i;
+        const uint32_t f = *px_flag<M, C>(bk, j);
+        float v[C];
+        bool valid = (f & 0xffu) != 0;  // uninitialised pixels are seeded, not matched
+        if constexpr (C == 3) {
+            v[0] = (float)r[i];
+            v[1] = (float)g[i];
+            v[2] = (float)b[i];
+        } else {
+            const uint32_t raw = d[i];
+            valid = valid && raw != 0;  // no return: no step (segmenter.cpp:84,128)
+            v[0] = (float)raw;
+        }
+        if (valid) {
+            const float* s = px_base<M, C>(bk, j);
+#pragma unroll
+            for (int q = 0; q < M; ++q) {
+                const float band = fmul(lambda, fsqrt(s[(M * C + q) * kBlockPx]));
+                const float tol = fmul(rel, band);
+#pragma unroll
+                for (int c = 0; c < C; ++c) {
+                    const float dist = fabsf(fsub(v[c], s[(q * C + c) * kBlockPx]));
+                    near = near || fabsf(fsub(dist, band)) <= tol;
+                }
+            }
+        }
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, near);
+    if ((threadIdx.x & 31) == 0 && bal) atomicAdd(count, (unsigned long long)__popc(bal));
 }
 
 // ---------------------------------------------------------------- K1b banks
@@ -721,6 +780,73 @@ __global__ void k_mix_step(PixRec* recs, const float* values, int channels, size
     }
     if (lab != 255) recs[j] = rec;
     labels[j] = lab;
+}
+
+// match_component / classify / update_mixture on their own (mixture.hpp:45-56).
+template <int M, int C>
+__device__ void rec_op(PixRec& rec, const float* vals, const MixCfg& k, int op, int& matched,
+                       uint8_t& lab) {
+    Mixture<M, C> m;
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+#pragma unroll
+        for (int c = 0; c < C; ++c) m.mu[i][c] = rec.means[i * C + c];
+        m.var[i] = rec.variances[i];
+        m.w[i] = rec.weights[i];
+    }
+    float v[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) v[c] = vals ? vals[c] : 0.0f;
+    if (op == kOpMatch) {
+        matched = gmm_match(m, v, k);
+        lab = 0;
+    } else if (op == kOpClassify) {
+        lab = (uint8_t)gmm_classify(m, matched, k);
+    } else {
+        gmm_update(m, v, matched, k);
+        lab = 0;
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+#pragma unroll
+            for (int c = 0; c < C; ++c) rec.means[i * C + c] = m.mu[i][c];
+            rec.variances[i] = m.var[i];
+            rec.weights[i] = m.w[i];
+        }
+    }
+}
+
+template <int M>
+__device__ void rec_op_c(PixRec& rec, const float* vals, const MixCfg& k, int op, int& matched,
+                         uint8_t& lab) {
+    switch (rec.channels) {
+        case 1: rec_op<M, 1>(rec, vals, k, op, matched, lab); break;
+        case 2: rec_op<M, 2>(rec, vals, k, op, matched, lab); break;
+        case 3: rec_op<M, 3>(rec, vals, k, op, matched, lab); break;
+        case 4: rec_op<M, 4>(rec, vals, k, op, matched, lab); break;
+        default: lab = 255; break;
+    }
+}
+
+// values: n * rec.channels floats (NULL for classify); matched: in for
+// classify / update, out for match; labels: classify's result (255 = bad
+// record shape, which the host rejects before launching).
+__global__ void k_mix_op(PixRec* recs, const float* values, size_t n, MixCfg k, int op,
+                         int* matched, uint8_t* labels) {
+    const size_t j = (size_t)blockIdx.x * kThreads + threadIdx.x;
+    if (j >= n) return;
+    PixRec rec = recs[j];
+    int mt = op == kOpMatch ? -1 : matched[j];
+    uint8_t lab = 255;
+    const float* v = values ? values + j * rec.channels : nullptr;
+    switch (rec.components) {
+        case 3: rec_op_c<3>(rec, v, k, op, mt, lab); break;
+        case 4: rec_op_c<4>(rec, v, k, op, mt, lab); break;
+        case 5: rec_op_c<5>(rec, v, k, op, mt, lab); break;
+        default: break;
+    }
+    if (op == kOpMatch) matched[j] = mt;
+    if (op == kOpClassify && labels) labels[j] = lab;
+    if (op == kOpUpdate && lab != 255) recs[j] = rec;
 }
 
 __global__ void k_mix_init(const float* values, int channels, size_t n, MixCfg k, int M,
@@ -971,12 +1097,17 @@ template <int MC, int MD>
 cudaError_t fused_ldg_md(const FusedArgs& a, bool elide, cudaStream_t s) {
     if (a.n == 0) return cudaSuccess;
     const unsigned nb = blocks_for(a.n);
-    if (elide)
+    if (a.packed) {  // interleaved colour input (no evaluation epilogue)
+        if (a.gt) return cudaErrorInvalidValue;
+        elide ? k_fused_ldg<MC, MD, true, false, true><<<nb, kThreads, 0, s>>>(a)
+              : k_fused_ldg<MC, MD, false, false, true><<<nb, kThreads, 0, s>>>(a);
+    } else if (elide) {
         a.gt ? k_fused_ldg<MC, MD, true, true><<<nb, kThreads, 0, s>>>(a)
              : k_fused_ldg<MC, MD, true, false><<<nb, kThreads, 0, s>>>(a);
-    else
+    } else {
         a.gt ? k_fused_ldg<MC, MD, false, true><<<nb, kThreads, 0, s>>>(a)
              : k_fused_ldg<MC, MD, false, false><<<nb, kThreads, 0, s>>>(a);
+    }
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return cudaGetLastError();
 }
@@ -1035,6 +1166,24 @@ cudaError_t launch_fused(const FusedArgs& a, int variant, cudaStream_t s) {
         case 5: return fused_mc<5>(a, variant, s);
     }
     return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_near(const FusedArgs& a, float rel, unsigned long long* counts, cudaStream_t s) {
+    if (a.n == 0) return cudaSuccess;
+    const unsigned nb = blocks_for(a.n);
+    const float lc = a.ck.lambda, ld = a.dk.lambda;
+    switch (a.color.M) {
+        case 3: k_near<3, 3><<<nb, kThreads, 0, s>>>(a.color, a.r, a.g, a.b, a.d, a.base, a.n, lc, rel, counts); break;
+        case 4: k_near<4, 3><<<nb, kThreads, 0, s>>>(a.color, a.r, a.g, a.b, a.d, a.base, a.n, lc, rel, counts); break;
+        default: k_near<5, 3><<<nb, kThreads, 0, s>>>(a.color, a.r, a.g, a.b, a.d, a.base, a.n, lc, rel, counts); break;
+    }
+    switch (a.depth.M) {
+        case 3: k_near<3, 1><<<nb, kThreads, 0, s>>>(a.depth, a.r, a.g, a.b, a.d, a.base, a.n, ld, rel, counts + 1); break;
+        case 4: k_near<4, 1><<<nb, kThreads, 0, s>>>(a.depth, a.r, a.g, a.b, a.d, a.base, a.n, ld, rel, counts + 1); break;
+        default: k_near<5, 1><<<nb, kThreads, 0, s>>>(a.depth, a.r, a.g, a.b, a.d, a.base, a.n, ld, rel, counts + 1); break;
+    }
+    g_launches.fetch_add(2, std::memory_order_relaxed);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_bank_color(BankView bk, const MixCfg& k, const uint8_t* r, const uint8_t* g,
@@ -1097,6 +1246,11 @@ cudaError_t launch_mix_init(const float* values, int channels, size_t n, const M
 cudaError_t launch_mix_step(PixRec* recs, const float* values, int channels, size_t n,
                             const MixCfg& k, uint8_t* labels, cudaStream_t s) {
     return go(k_mix_step, n, s, recs, values, channels, n, k, labels);
+}
+
+cudaError_t launch_mix_op(PixRec* recs, const float* values, size_t n, const MixCfg& k, int op,
+                          int* matched, uint8_t* labels, cudaStream_t s) {
+    return go(k_mix_op, n, s, recs, values, n, k, op, matched, labels);
 }
 
 cudaError_t launch_render(const SceneFrame& sc, uint8_t* r, uint8_t* g, uint8_t* b, uint16_t* d,

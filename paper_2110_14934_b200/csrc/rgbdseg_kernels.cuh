@@ -79,6 +79,11 @@ struct FusedArgs {
     // L2 prefetch distance in thread blocks (0 = off): each warp prefetches
     // the bank tiles of the warp `ahead` blocks later (~one occupancy wave)
     unsigned ahead;
+    // interleaved colour input: `r` is ONE plane of 3 bytes per pixel
+    // (pre-offset by 3*base), R,G,B order (bgr = 0) or B,G,R (bgr = 1);
+    // g and b are unused.  Not combined with the evaluation epilogue.
+    int packed;
+    int bgr;
 };
 
 // Kernel variants of K1 (identical results; they differ in HBM writes).
@@ -88,6 +93,11 @@ enum Variant { kAuto = 0, kLdgDense = 1, kLdgElide = 2 };
 
 // All launchers return cudaGetLastError() after the launch.
 cudaError_t launch_fused(const FusedArgs& a, int variant, cudaStream_t s);
+// Near-threshold report (diagnostic, read-only): adds to counts[0] the colour
+// pixels and to counts[1] the depth pixels of launch `a` whose observation
+// lies within rel * lambda*sigma of a component's match band, on the state
+// before the step.  Launch it before launch_fused(a) on the same stream.
+cudaError_t launch_near(const FusedArgs& a, float rel, unsigned long long* counts, cudaStream_t s);
 cudaError_t launch_bank_color(BankView bank, const MixCfg& k, const uint8_t* r, const uint8_t* g,
                               const uint8_t* b, uint8_t* mask, size_t n, cudaStream_t s);
 cudaError_t launch_bank_depth(BankView bank, const MixCfg& k, const uint16_t* d, uint8_t* mask,
@@ -116,6 +126,14 @@ cudaError_t launch_mix_init(const float* values, int channels, size_t n, const M
 // labels: 0/1, or 255 for a record whose shape the kernel cannot step.
 cudaError_t launch_mix_step(PixRec* recs, const float* values, int channels, size_t n,
                             const MixCfg& k, uint8_t* labels, cudaStream_t s);
+
+// match_component / classify / update_mixture batched over records
+// (mixture.hpp:45-56): op kOpMatch writes matched[j] (-1 = no match),
+// kOpClassify reads matched[j] and writes labels[j] (1 = FG), kOpUpdate
+// reads matched[j] and values (n * channels) and updates the record.
+enum { kOpMatch = 0, kOpClassify = 1, kOpUpdate = 2 };
+cudaError_t launch_mix_op(PixRec* recs, const float* values, size_t n, const MixCfg& k, int op,
+                          int* matched, uint8_t* labels, cudaStream_t s);
 
 // Synthetic scene for one frame (frame-level quantities resolved on the host).
 struct SceneFrame {

@@ -250,6 +250,84 @@ def step_pixel(mix: PixelMixture, value, cfg: MixtureConfig) -> int:
     return int(lab[0])
 
 
+def _recs_values(recs, values):
+    if recs.dtype != PIXEL_MIXTURE_DTYPE or not recs.flags.c_contiguous:
+        raise ValueError("records must be a contiguous PIXEL_MIXTURE_DTYPE array")
+    n = recs.size
+    v = np.ascontiguousarray(values, dtype=np.float32)
+    if v.ndim == 1:
+        v = v.reshape(n, -1)
+    if v.shape[0] != n:
+        raise ValueError("one observation per record expected")
+    return n, v
+
+
+def _matched_array(matched, n):
+    m = np.ascontiguousarray(
+        [-1 if x is None else int(x) for x in matched] if isinstance(matched, (list, tuple))
+        else matched, dtype=np.int32).reshape(-1)
+    if m.size != n:
+        raise ValueError("one matched index per record expected")
+    return m
+
+
+def match_components(recs: np.ndarray, values, cfg: MixtureConfig, device: int = 0) -> np.ndarray:
+    """Batched match_component (mixture.cpp:74-92) on the GPU: int32 index of
+    each record's matched component, -1 for none (std::nullopt)."""
+    n, v = _recs_values(recs, values)
+    out = np.empty(n, np.int32)
+    c = cfg._c()
+    check(lib.rgbdseg_match_components(recs.ctypes.data, v.ctypes.data, v.shape[1], n,
+                                       C.byref(c), out.ctypes.data, device))
+    return out
+
+
+def classify_mixtures(recs: np.ndarray, matched, cfg: MixtureConfig, device: int = 0) -> np.ndarray:
+    """Batched classify (mixture.cpp:133-146) on the GPU: uint8 labels (1 = FG)."""
+    if recs.dtype != PIXEL_MIXTURE_DTYPE or not recs.flags.c_contiguous:
+        raise ValueError("records must be a contiguous PIXEL_MIXTURE_DTYPE array")
+    n = recs.size
+    m = _matched_array(matched, n)
+    out = np.empty(n, np.uint8)
+    c = cfg._c()
+    check(lib.rgbdseg_classify_mixtures(recs.ctypes.data, m.ctypes.data, n, C.byref(c),
+                                        out.ctypes.data, device))
+    return out
+
+
+def update_mixtures(recs: np.ndarray, values, matched, cfg: MixtureConfig, device: int = 0):
+    """Batched update_mixture (mixture.cpp:94-131) on the GPU, in place."""
+    n, v = _recs_values(recs, values)
+    m = _matched_array(matched, n)
+    c = cfg._c()
+    check(lib.rgbdseg_update_mixtures(recs.ctypes.data, v.ctypes.data, v.shape[1], n,
+                                      m.ctypes.data, C.byref(c), device))
+
+
+def match_component(mix: PixelMixture, value, cfg: MixtureConfig) -> Optional[int]:
+    """match_component (mixture.hpp:45-48): index of the first component, in
+    decreasing w/sigma order, within lambda*sigma in every channel; None if
+    there is none."""
+    v = np.asarray(list(value), dtype=np.float32)
+    if v.size != mix.channels:
+        raise ValueError("match_component: observation dimensionality does not match the mixture")
+    i = int(match_components(mix._rec.reshape(1), v[None, :], cfg)[0])
+    return None if i < 0 else i
+
+
+def classify(mix: PixelMixture, matched: Optional[int], cfg: MixtureConfig) -> int:
+    """classify (mixture.hpp:53-56): 1 = Foreground, 0 = Background."""
+    return int(classify_mixtures(mix._rec.reshape(1), [matched], cfg)[0])
+
+
+def update_mixture(mix: PixelMixture, value, matched: Optional[int], cfg: MixtureConfig) -> None:
+    """update_mixture (mixture.hpp:50-51), in place."""
+    v = np.asarray(list(value), dtype=np.float32)
+    if v.size != mix.channels:
+        raise ValueError("update_mixture: observation dimensionality does not match the mixture")
+    update_mixtures(mix._rec.reshape(1), v[None, :], [matched], cfg)
+
+
 # ------------------------------------------------------------------ banks
 
 class BankMode:
@@ -621,6 +699,18 @@ class SequenceProcessor:
         return (self.height, self.width) if self.streams == 1 else (
             self.streams, self.height, self.width)
 
+    def set_near_threshold(self, rel: float = 1e-5):
+        """Turn on (rel > 0) or off (0) the near-threshold report and zero
+        its counters (see rgbdseg_processor_set_near_threshold)."""
+        check(lib.rgbdseg_processor_set_near_threshold(self._h, float(rel)))
+
+    def near_threshold_counts(self) -> dict:
+        """{'color': n, 'depth': n, 'pixel_frames': n} since set_near_threshold."""
+        c, d, n = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        check(lib.rgbdseg_processor_near_threshold_counts(self._h, C.byref(c), C.byref(d),
+                                                          C.byref(n)))
+        return {"color": c.value, "depth": d.value, "pixel_frames": n.value}
+
     def set_variant(self, variant: str):
         check(lib.rgbdseg_processor_set_variant(self._h, _lib.VARIANTS[variant]))
 
@@ -676,6 +766,44 @@ class SequenceProcessor:
                                                  counts.ctypes.data, *ptrs[4:]), "process")
         return FrameMasks(idx, out.get("rgb"), out.get("depth"), out.get("fused"), counts)
 
+    def _packed_args(self, rgb, depth, order, fused, rgbm, depm):
+        n = self.npx
+        if order not in ("rgb", "bgr"):
+            raise ValueError("order must be 'rgb' or 'bgr'")
+        shp = self._shape()
+        rgb = _as_host(rgb, np.uint8, (*shp, 3))
+        depth = _as_host(depth, np.uint16, shp)
+        ptrs = [_buf(rgb, np.uint8, 3 * n, "process(rgb interleaved)"),
+                _lib.ORDER[order], _buf(depth, np.uint16, n, "process(depth)"),
+                _buf(fused, np.uint8, n, "fused", True), _buf(rgbm, np.uint8, n, "rgb", True),
+                _buf(depm, np.uint8, n, "depth_mask", True)]
+        return ptrs, (rgb, depth)
+
+    def process_interleaved(self, rgb, depth, order: str = "rgb",
+                            want=("rgb", "depth", "fused"), out=None) -> FrameMasks:
+        """process() from an interleaved colour frame (H, W, 3) or
+        (streams, H, W, 3) -- R,G,B (aos_to_soa's layout, engine.cpp:39-56)
+        or B,G,R (OpenCV / Kinect order); the kernel deinterleaves it."""
+        out = dict(out or {})
+        for k in want:
+            if k not in out:
+                out[k] = np.empty(self._shape(), np.uint8)
+        ptrs, keep = self._packed_args(rgb, depth, order, out.get("fused"), out.get("rgb"),
+                                       out.get("depth"))
+        _finish_producers(*keep, out.get("fused"), out.get("rgb"), out.get("depth"))
+        idx = self.frames
+        check(lib.rgbdseg_processor_process_interleaved(self._h, *ptrs), "process_interleaved")
+        return FrameMasks(idx, out.get("rgb"), out.get("depth"), out.get("fused"))
+
+    def submit_interleaved(self, rgb, depth, order: str = "rgb", fused=None, rgb_mask=None,
+                           depth_mask=None):
+        """submit() from an interleaved colour frame (see process_interleaved);
+        buffers must stay alive until sync()."""
+        ptrs, keep = self._packed_args(rgb, depth, order, fused, rgb_mask, depth_mask)
+        self._keep.append((keep, fused, rgb_mask, depth_mask))
+        _finish_producers(*keep, fused, rgb_mask, depth_mask)
+        check(lib.rgbdseg_processor_submit_interleaved(self._h, *ptrs), "submit_interleaved")
+
     def submit(self, r, g, b, depth, fused=None, rgb=None, depth_mask=None, order=True):
         """Enqueue one step without waiting; buffers must stay alive and
         unmodified until ``sync()``.  With CUDA tensors and ``order`` the step
@@ -697,6 +825,30 @@ class SequenceProcessor:
     def sync(self):
         check(lib.rgbdseg_processor_sync(self._h), "sync")
         self._keep.clear()
+
+
+# ------------------------------------------------------------------ layout helpers
+
+def aos_to_soa(frame):
+    """aos_to_soa (engine.cpp:39-56; module.cpp:121-131): an interleaved
+    H x W x 3 uint8 frame -> (r, g, b) planes.  The GPU path does not need
+    it (SequenceProcessor.process_interleaved deinterleaves in the kernel)."""
+    a = np.asarray(frame)
+    if a.ndim != 3 or a.shape[2] != 3:
+        raise ValueError("expected an HxWx3 array")
+    a = np.ascontiguousarray(a, dtype=np.uint8)
+    return tuple(np.ascontiguousarray(a[:, :, c]) for c in range(3))
+
+
+def soa_to_aos(r, g, b):
+    """soa_to_aos (engine.cpp:58-74): three planes -> interleaved H x W x 3."""
+    planes = [np.asarray(x, dtype=np.uint8) for x in (r, g, b)]
+    for p in planes[1:]:
+        if p.shape != planes[0].shape:
+            h0, w0 = planes[0].shape[-2:]
+            h1, w1 = p.shape[-2:]
+            raise ValueError(f"soa_to_aos: dimension mismatch ({w0}x{h0} vs {w1}x{h1})")
+    return np.ascontiguousarray(np.stack(planes, axis=-1))
 
 
 # ------------------------------------------------------------------ evaluation

@@ -45,14 +45,24 @@ def test_library_is_sm100a_only():
     assert arches == {"sm_100a"}, arches
 
 
-def _ptx(tmp_path, fmad: str) -> str:
-    ptx = tmp_path / f"k_{fmad}.ptx"
+def _ptx_pair(tmp_path):
+    """PTX of the kernels under -fmad=false and -fmad=true (two nvcc runs in
+    parallel)."""
     src = os.path.join(ROOT, "paper_2110_14934_b200", "csrc", "rgbdseg_kernels.cu")
-    r = subprocess.run(["nvcc", "-arch=sm_100a", "-ptx", "-std=c++17", f"-fmad={fmad}",
-                        "-prec-div=true", "-prec-sqrt=true", "-ftz=false", src, "-o", str(ptx)],
-                       capture_output=True, text=True)
-    assert r.returncode == 0, r.stderr
-    return "\n".join(ln for ln in ptx.read_text().splitlines() if not ln.startswith("//"))
+    runs = {}
+    for fmad in ("false", "true"):
+        ptx = tmp_path / f"k_{fmad}.ptx"
+        runs[fmad] = (ptx, subprocess.Popen(
+            ["nvcc", "-arch=sm_100a", "-ptx", "-std=c++17", f"-fmad={fmad}", "-prec-div=true",
+             "-prec-sqrt=true", "-ftz=false", src, "-o", str(ptx)],
+            stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True))
+    out = []
+    for fmad in ("false", "true"):
+        ptx, pr = runs[fmad]
+        _, err = pr.communicate()
+        assert pr.returncode == 0, err
+        out.append("\n".join(ln for ln in ptx.read_text().splitlines() if not ln.startswith("//")))
+    return out
 
 
 def test_hot_kernels_have_no_contractible_arithmetic(tmp_path):
@@ -61,12 +71,13 @@ def test_hot_kernels_have_no_contractible_arithmetic(tmp_path):
     intrinsic, so the PTX must be byte-identical under -fmad=false and
     -fmad=true; the only FMAs are the explicit ones inside the exact
     division / square-root sequences of gmm_step_fast."""
-    strict, loose = _ptx(tmp_path, "false"), _ptx(tmp_path, "true")
+    strict, loose = _ptx_pair(tmp_path)
 
     def gmm_entries(ptx):  # the GMM / fusion kernels (not the scene generator)
         parts = re.split(r"(?=\.(?:visible )?\.?entry )", ptx)
         keep = [p for p in parts if re.match(r"\.(?:visible )?\.?entry ", p)
-                and re.search(r"k_(fused_ldg|bank_color|bank_depth|mix_step|fuse)", p.split("(")[0])]
+                and re.search(r"k_(fused_ldg|bank_color|bank_depth|bank_aug|mix_step|mix_op|fuse|near)",
+                                 p.split("(")[0])]
         return keep
 
     a, b = gmm_entries(strict), gmm_entries(loose)
@@ -121,3 +132,23 @@ def test_default_config_json_matches_reference_defaults():
     assert cfg["depth_gmm"]["learning_rate"] == pytest.approx(0.01)
     assert cfg["depth_gmm"]["initial_sigma"] == 100.0
     assert cfg["fusion"] == {"counter_limit": 3, "initial_label": 0}
+
+
+def test_aos_soa_helpers_match_reference_layout():
+    """aos_to_soa / soa_to_aos (engine.cpp:39-74, module.cpp:121-131): R,G,B
+    interleaved <-> planes, the reference's errors."""
+    import numpy as np
+
+    import paper_2110_14934_b200 as R
+
+    rng = np.random.default_rng(1)
+    f = rng.integers(0, 256, (7, 5, 3), dtype=np.uint8)
+    r, g, b = R.aos_to_soa(f)
+    flat = f.reshape(-1)
+    assert np.array_equal(r.ravel(), flat[0::3]) and np.array_equal(g.ravel(), flat[1::3])
+    assert np.array_equal(b.ravel(), flat[2::3])
+    assert np.array_equal(R.soa_to_aos(r, g, b), f)
+    with pytest.raises(ValueError, match="HxWx3"):
+        R.aos_to_soa(np.zeros((4, 4), np.uint8))
+    with pytest.raises(ValueError, match="soa_to_aos: dimension mismatch"):
+        R.soa_to_aos(r, g, np.zeros((3, 3), np.uint8))

@@ -115,6 +115,70 @@ def test_scalar_api_smoke(R):
     assert R.step_pixel(mix, [250.0], cfg) == 1
 
 
+def test_match_classify_update_batched_vs_oracle(R, port):
+    """match_component / classify / update_mixture through the C-ABI
+    (mixture.hpp:45-56) on the GPU vs the oracle, bitwise: random
+    mid-sequence mixtures, values on the band edge, every matched index
+    (incl. none) for classify and update, NaN / zero weights."""
+    import ctypes as C
+
+    rng = np.random.default_rng(3)
+    L = port.lib
+    for M in (3, 4, 5):
+        for Ch in (1, 3, 4):
+            oc = O.color_cfg(M, learning_rate=0.07, background_threshold=0.75)
+            cfg = rcfg(R, oc)
+            mixes, vals = [], []
+            for t in range(600):
+                m = port.init_mixture(rng.uniform(0, 255, Ch).astype(np.float32), oc)
+                for _ in range(t % 23):
+                    port.step_pixel(m, rng.uniform(0, 255, Ch).astype(np.float32), oc)
+                v = rng.uniform(0, 255, Ch).astype(np.float32)
+                if t % 5 == 1:  # exactly on component 0's band edge
+                    band = np.float32(oc.match_lambda) * np.sqrt(np.float32(m.variances[0]),
+                                                                 dtype=np.float32)
+                    v = (np.float32(m.means[0]) + band).astype(np.float32) * np.ones(Ch, np.float32)
+                if t % 97 == 3:
+                    m.weights[1] = float("nan")
+                if t % 89 == 5:
+                    m.weights[0] = 0.0
+                mixes.append(m)
+                vals.append(v)
+            recs = np.frombuffer(b"".join(bytes(m) for m in mixes), R.PIXEL_MIXTURE_DTYPE).copy()
+            V = np.stack(vals)
+            got = R.match_components(recs, V, cfg)
+            exp = [L.orc_match(C.byref(m), v, C.byref(oc)) for m, v in zip(mixes, vals)]
+            assert got.tolist() == exp, (M, Ch)
+            for mt in [got] + [np.full(len(mixes), k, np.int32) for k in range(-1, M)]:
+                lab = R.classify_mixtures(recs, mt, cfg)
+                exp = [L.orc_classify(C.byref(m), int(k), C.byref(oc)) for m, k in zip(mixes, mt)]
+                assert lab.tolist() == exp, (M, Ch)
+            mt = rng.integers(-1, M, len(mixes)).astype(np.int32)
+            upd = recs.copy()
+            R.update_mixtures(upd, V, mt, cfg)
+            for k, (m, v) in enumerate(zip(mixes, vals)):
+                x = O.Mix.from_buffer_copy(m)
+                L.orc_update(C.byref(x), v, int(mt[k]), C.byref(oc))
+                assert bytes(x) == upd[k].tobytes(), (M, Ch, k)
+    # scalar API: test_mixture.cpp:70-85 (band 20 < 25 / 30 > 25), :121-134
+    c = R.MixtureConfig()
+    mix = R.init_mixture([100.0], c)
+    mix.raw()["variances"][0] = 100.0
+    assert R.match_component(mix, [120.0], c) == 0
+    assert R.match_component(mix, [130.0], c) is None
+    m2 = R.init_mixture([10.0], c)
+    m2.raw()["weights"][:3] = [0.7, 0.2, 0.1]
+    m2.raw()["variances"][:3] = 25.0
+    assert [R.classify(m2, k, c) for k in (2, 1, 0, None)] == [1, 0, 0, 1]
+    m3 = R.init_mixture([50.0], R.MixtureConfig(learning_rate=0.1))
+    m3.raw()["weights"][:3] = [0.5, 0.3, 0.2]
+    m3.raw()["means"][1:3] = 50.0
+    R.update_mixture(m3, [50.0], 0, R.MixtureConfig(learning_rate=0.1))
+    assert np.allclose(m3.weights, [0.55, 0.27, 0.18], rtol=1e-5)
+    with pytest.raises(ValueError, match="matched index"):
+        R.update_mixture(m3, [50.0], 3, c)
+
+
 # ------------------------------------------------------------ banks (K1b)
 
 def test_segment_color_soa_transparency(R, port):
@@ -281,6 +345,107 @@ def test_processor_multistream_device_vs_oracle(R, port, cuda, variant):
     P = proc.color_bank().planes().reshape(-1, S, w * h)
     for s in range(S):
         assert P[:, s].tobytes() == orc[s].color.planes().tobytes()
+
+
+def _near_count_np(bank, vals, lam, rel, valid):
+    """Near-threshold pixels of an oracle bank (flat planes) for
+    observations vals[C, npx]: | |v - mu| - lambda*sigma | <= rel*lambda*sigma
+    in any channel of any component, fp32 round-to-nearest like the kernel."""
+    P = bank.planes()
+    M, Ch = bank.cfg.components, bank.channels
+    near = np.zeros(P.shape[1], bool)
+    for i in range(M):
+        band = np.float32(lam) * np.sqrt(P[M * Ch + i], dtype=np.float32)
+        tol = np.float32(rel) * band
+        for c in range(Ch):
+            dist = np.abs(vals[c] - P[i * Ch + c])
+            near |= np.abs(dist - band) <= tol
+    return int((near & valid & (bank.flags != 0)).sum())
+
+
+@pytest.mark.parametrize("rel", [1e-5, 2e-3])
+def test_near_threshold_report_matches_oracle_state(R, port, cuda, rel):
+    """The processor's near-threshold report (north_star: pixels within
+    rel*lambda*sigma of the match band are counted and reported) equals the
+    count over the oracle's pre-step state, frame by frame; masks stay
+    bitwise equal while it runs."""
+    w, h, S, M = 96, 64, 2, 5
+    cfg = R.RunConfig.defaults()
+    cfg.color_gmm.components = cfg.depth_gmm.components = M
+    proc = R.SequenceProcessor(w, h, cfg, streams=S)
+    proc.set_near_threshold(rel)
+    npx = S * w * h
+    orc = O.PortProcessor(port, npx, O.color_cfg(M), O.depth_cfg(M))
+    scenes = [O.PortScene(port, "A", w, h, seed=s + 1) for s in range(S)]
+    exp_c = exp_d = 0
+    for f in range(40):
+        frs = [sc.render(90 + f) for sc in scenes]
+        r, g, b = (np.stack([getattr(x, k) for x in frs]) for k in ("r", "g", "b"))
+        d = np.stack([holes(x.depth, f) for x in frs])
+        rgbv = np.stack([r.ravel(), g.ravel(), b.ravel()]).astype(np.float32)
+        dv = d.ravel().astype(np.float32)[None]
+        exp_c += _near_count_np(orc.color, rgbv, 2.5, rel, np.ones(npx, bool))
+        exp_d += _near_count_np(orc.depth, dv, 2.5, rel, d.ravel() != 0)
+        fm = proc.process(r, g, b, d)
+        _, _, fu = orc.process(r.ravel(), g.ravel(), b.ravel(), d.ravel())
+        assert np.array_equal(fm.fused.ravel(), fu), f
+    got = proc.near_threshold_counts()
+    print("near-threshold", rel, got, exp_c, exp_d)
+    assert got == {"color": exp_c, "depth": exp_d, "pixel_frames": 40 * npx}
+    if rel > 1e-4:
+        assert exp_c > 0
+    proc.set_near_threshold(0.0)
+
+
+@pytest.mark.parametrize("w,h,S,chunks", [(96, 64, 2, 0), (37, 23, 3, 0), (160, 120, 4, 3)])
+def test_interleaved_ingest_matches_planar(R, port, cuda, w, h, S, chunks):
+    """process_interleaved: an R,G,B- or B,G,R-interleaved colour frame
+    (aos_to_soa's layout, engine.cpp:39-56) deinterleaved inside K1 gives the
+    planar path's masks and banks bit for bit -- host frames (packed+depth in
+    one buffer, and separate), device frames, odd sizes, chunked uploads."""
+    import torch
+
+    M = 5
+    cfg = R.RunConfig.defaults()
+    cfg.color_gmm.components = cfg.depth_gmm.components = M
+    procs = {k: R.SequenceProcessor(w, h, cfg, streams=S, host_chunks=chunks)
+             for k in ("planar", "rgb", "bgr", "dev")}
+    orc = O.PortProcessor(port, S * w * h, O.color_cfg(M), O.depth_cfg(M))
+    scenes = [O.PortScene(port, "A", w, h, seed=s + 1) for s in range(S)]
+    for f in range(24):
+        frs = [sc.render(100 + f) for sc in scenes]
+        r, g, b = (np.stack([getattr(x, k) for x in frs]) for k in ("r", "g", "b"))
+        d = np.stack([holes(x.depth, f) for x in frs])
+        rgb = R.soa_to_aos(r, g, b)
+        bgr = np.ascontiguousarray(rgb[..., ::-1])
+        res = {"planar": procs["planar"].process(r, g, b, d)}
+        if f % 2:  # packed colour + depth in one host buffer
+            buf = np.empty(S * w * h * 5, np.uint8)
+            buf[:3 * S * w * h] = rgb.ravel()
+            buf[3 * S * w * h:].view(np.uint16)[:] = d.ravel()
+            prgb = buf[:3 * S * w * h].reshape(S, h, w, 3)
+            pd = buf[3 * S * w * h:].view(np.uint16).reshape(S, h, w)
+            res["rgb"] = procs["rgb"].process_interleaved(prgb, pd, "rgb")
+        else:
+            res["rgb"] = procs["rgb"].process_interleaved(rgb, d, "rgb")
+        res["bgr"] = procs["bgr"].process_interleaved(bgr, d, "bgr")
+        dev = torch.device("cuda", 0)
+        trgb = torch.from_numpy(rgb).to(dev)
+        td = torch.from_numpy(d.view(np.int16)).to(dev).view(torch.uint16)
+        outs = {k: torch.empty((S, h, w), dtype=torch.uint8, device=dev)
+                for k in ("rgb", "depth", "fused")}
+        procs["dev"].process_interleaved(trgb, td, "rgb", out=outs)
+        res["dev"] = R.FrameMasks(f, *(outs[k].cpu().numpy() for k in ("rgb", "depth", "fused")))
+        ergb, edep, efu = orc.process(r.ravel(), g.ravel(), b.ravel(), d.ravel())
+        for k, fm in res.items():
+            assert np.array_equal(np.asarray(fm.rgb).ravel(), ergb), (k, f)
+            assert np.array_equal(np.asarray(fm.depth).ravel(), edep), (k, f)
+            assert np.array_equal(np.asarray(fm.fused).ravel(), efu), (k, f)
+    for k, p in procs.items():
+        assert p.color_bank().planes().tobytes() == orc.color.planes().tobytes(), k
+        assert p.depth_bank().planes().tobytes() == orc.depth.planes().tobytes(), k
+    with pytest.raises(ValueError, match="order"):
+        procs["rgb"].process_interleaved(rgb, d, "gbr")
 
 
 def test_host_chunked_pipeline_equals_device_path(R, cuda):
@@ -1212,3 +1377,90 @@ def test_pipelined_single_chunk_submits_deliver_every_frame(R, cuda):
         assert np.array_equal(o["fused"], ef), f
         assert np.array_equal(o["rgb"], er), f
         assert np.array_equal(o["depth_mask"], ed), f
+
+
+# ------------------------------------------------ BASELINE configs at their shape
+
+def _gpu_frame_host(R, w, h, f, holes_on=True):
+    """Scenario A frame `f` at w x h rendered on the GPU (K3) and copied to
+    the host: the CPU reference and the GPU path consume the same bytes."""
+    fr = R.render_scenario("A", w, h, f, streams=1)
+    r, g, b = (to_np(fr[k])[0] for k in ("r", "g", "b"))
+    d = to_np(fr["depth"])[0]
+    return r, g, b, (holes(d, f) if holes_on else d)
+
+
+def _ref_plane(ref, rp, which, kind, i, c, n, dtype=np.float32):
+    out = np.empty(n, dtype)
+    ref.check(ref.lib.rref_processor_bank_get(rp.p, which, kind, i, c, out.ctypes.data))
+    return out
+
+
+def _check_banks_vs_ref(ref, rp, banks, n, M):
+    """Every plane and the flags of the GPU banks (a list of (bank, row
+    slice) tiles covering the frame) against the reference processor's,
+    one plane at a time."""
+    for which, Ch in ((0, 3), (1, 1)):
+        planes = [(0, i, c) for i in range(M) for c in range(Ch)]
+        planes += [(1, i, 0) for i in range(M)] + [(2, i, 0) for i in range(M)]
+        for pid, (kind, i, c) in enumerate(planes):
+            exp = _ref_plane(ref, rp, which, kind, i, c, n)
+            got = np.concatenate([bk[which].download_plane(pid).reshape(-1) for bk in banks])
+            assert got.tobytes() == exp.tobytes(), (which, kind, i, c)
+        exp = _ref_plane(ref, rp, which, 3, 0, 0, n, np.uint8)
+        got = np.concatenate([bk[which].initialized_plane().reshape(-1) for bk in banks])
+        assert np.array_equal(got, exp), which
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="compiled reference (oracle/_ref) absent")
+def test_config3_1080p_full_sequence_vs_reference(R, cuda):
+    """BASELINE configs[2] at its shape: 1920x1080, M=5, all 300 frames of
+    scenario A -- 1.5x illumination step [100,112), 0.6x dip [200,212),
+    shadow [150,180), flicker -- plus depth holes, against the reference's
+    own SequenceProcessor on all host cores (oracle/_ref).  rgb, depth and
+    fused masks (the fused mask is the fusion state's `out`) bitwise every
+    frame; final banks and flags bitwise."""
+    w, h, M = 1920, 1080, 5
+    ref = O.Ref()
+    rp = O.RefProcessor(ref, w, h, O.color_cfg(M), O.depth_cfg(M), workers=os.cpu_count() or 1)
+    cfg = R.RunConfig.defaults()
+    cfg.color_gmm.components = cfg.depth_gmm.components = M
+    proc = R.SequenceProcessor(w, h, cfg)
+    for f in range(300):
+        r, g, b, d = _gpu_frame_host(R, w, h, f)
+        fm = proc.process(r, g, b, d)
+        ergb, edep, efu = rp.process(r, g, b, d)
+        assert np.array_equal(fm.rgb.ravel(), ergb), f
+        assert np.array_equal(fm.depth.ravel(), edep), f
+        assert np.array_equal(fm.fused.ravel(), efu), f
+    _check_banks_vs_ref(ref, rp, [(proc.color_bank(), proc.depth_bank())], w * h, M)
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="compiled reference (oracle/_ref) absent")
+def test_config5_8k_full_frames_row_tiles_vs_reference(R, cuda):
+    """BASELINE configs[4] at its shape: the full 8192x8192 frame (not a
+    sample), M=5, processed as two row tiles (rows [0,4096) and [4096,8192),
+    the 2-GPU shard) against the reference on all host cores for 4 frames
+    (initialisation + 3 steps, depth holes): masks and every bank word."""
+    import torch
+
+    w = h = 8192
+    M = 5
+    ref = O.Ref()
+    rp = O.RefProcessor(ref, w, h, O.color_cfg(M), O.depth_cfg(M), workers=os.cpu_count() or 1)
+    cfg = R.RunConfig.defaults()
+    cfg.color_gmm.components = cfg.depth_gmm.components = M
+    tiles = [(0, 4096), (4096, 8192)]
+    procs = [R.SequenceProcessor(w, y1 - y0, cfg) for y0, y1 in tiles]
+    for f in (0, 97, 98, 99):
+        r, g, b, d = _gpu_frame_host(R, w, h, f)
+        ergb, edep, efu = rp.process(r, g, b, d)
+        for (y0, y1), p in zip(tiles, procs):
+            fm = p.process(*(np.ascontiguousarray(x[y0:y1]) for x in (r, g, b, d)))
+            sl = slice(y0 * w, y1 * w)
+            assert np.array_equal(fm.rgb.ravel(), ergb[sl]), (f, y0)
+            assert np.array_equal(fm.depth.ravel(), edep[sl]), (f, y0)
+            assert np.array_equal(fm.fused.ravel(), efu[sl]), (f, y0)
+        del r, g, b, d
+    torch.cuda.synchronize()
+    _check_banks_vs_ref(ref, rp, [(p.color_bank(), p.depth_bank()) for p in procs], w * h, M)

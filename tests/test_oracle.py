@@ -293,3 +293,29 @@ def test_port_augmented_matches_reference(port, ref):
         assert np.array_equal(pb.segment_augmented(fr.r, fr.g, fr.b, d), mr), f
     assert pb.planes().tobytes() == _ref_bank_planes(ref, bank, M, 4, w * h).tobytes()
     ref.lib.rref_bank_destroy(bank)
+
+
+def test_port_match_classify_update_vs_reference(port, ref):
+    """The three pieces of step_pixel on their own (mixture.hpp:45-56) --
+    match_component, classify with ANY matched index (incl. none), and
+    update_mixture with any matched index -- port vs the compiled reference,
+    bitwise, on random mid-sequence mixtures."""
+    rng = np.random.default_rng(11)
+    L = port.lib
+    for trial in range(1500):
+        M = 3 + trial % 3
+        Ch = (1, 3, 4)[trial % 3]
+        cfg = O.color_cfg(M, learning_rate=float(rng.uniform(0.005, 0.5)),
+                          background_threshold=float(rng.uniform(0.3, 0.95)))
+        m = port.init_mixture(rng.uniform(0, 255, Ch).astype(np.float32), cfg)
+        for _ in range(trial % 15):
+            port.step_pixel(m, rng.uniform(0, 255, Ch).astype(np.float32), cfg)
+        v = rng.uniform(0, 255, Ch).astype(np.float32)
+        a = O.Mix.from_buffer_copy(m)
+        assert L.orc_match(C.byref(a), v, C.byref(cfg)) == ref.match_component(a, v, cfg)
+        for mt in range(-1, M):
+            assert L.orc_classify(C.byref(a), mt, C.byref(cfg)) == ref.classify(a, mt, cfg)
+            x, y = O.Mix.from_buffer_copy(a), O.Mix.from_buffer_copy(a)
+            L.orc_update(C.byref(x), v, mt, C.byref(cfg))
+            ref.update_mixture(y, v, mt, cfg)
+            assert bytes(x) == bytes(y), (trial, mt)
