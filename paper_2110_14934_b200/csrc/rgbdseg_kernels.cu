@@ -345,9 +345,17 @@ __global__ void __launch_bounds__(kThreads)
 // initialised pixel, colour component 1 in most; a loaded untouched
 // component equals its substitute).  Only the rest waits for the flags.
 constexpr int kPre = RGBDSEG_PRE_COLOR;
+// Where K1 reads its fusion state (out, cpt): 0 = at List 1 (prefetched to
+// L1 in round one), 1 = right after the depth step, 2 = in round one.
+#ifndef RGBDSEG_FUSE_LOAD
+#define RGBDSEG_FUSE_LOAD 0
+#endif
 struct Round1 {
     float vc[3];
     uint32_t raw, cf, df;
+#if RGBDSEG_FUSE_LOAD == 2
+    uint32_t out0, cpt0;
+#endif
     Mixture<kPre, 3> cpre;
     Mixture<1, 1> dpre;
 };
@@ -413,6 +421,10 @@ __device__ __forceinline__ void fused_core(const FusedArgs& a, size_t i0, unsign
         if (df1 != r.df) st_h<kElide>(p.dflag(), (uint16_t)df1);
     }
 
+#if RGBDSEG_FUSE_LOAD == 1
+    const uint32_t out0 = a.fuse ? a.out[i0 + t] : 0u;
+    const int cpt0 = a.fuse ? (int)a.cpt[i0 + t] : 0;
+#endif
     // ---- colour stream (segment_color) ----
     const float vc[3] = {r.vc[0], r.vc[1], r.vc[2]};
     const Mixture<kPre, 3>& cpre = r.cpre;
@@ -424,8 +436,13 @@ __device__ __forceinline__ void fused_core(const FusedArgs& a, size_t i0, unsign
     if (cf1 != r.cf) st_h<kElide>(p.cflag(), (uint16_t)cf1);
 
     // ---- List-1 fusion on the registered depth mask ----
+#if RGBDSEG_FUSE_LOAD == 0
     const uint32_t out0 = a.fuse ? a.out[i0 + t] : 0u;  // L1 hits (plain loads)
     const int cpt0 = a.fuse ? (int)a.cpt[i0 + t] : 0;
+#elif RGBDSEG_FUSE_LOAD == 2
+    const uint32_t out0 = r.out0;
+    const int cpt0 = (int)(int8_t)r.cpt0;
+#endif
     uint32_t out = out0;
     int cpt = cpt0;
     if (a.fuse) {
@@ -465,10 +482,15 @@ __device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i0, unsig
     r.raw = ld_h<kElide>(a.d + i0 + t);
     r.cf = ld_h<kElide>(p.cflag());
     r.df = ld_h<kElide>(p.dflag());
+#if RGBDSEG_FUSE_LOAD == 2
+    r.out0 = a.fuse ? ld_h<kElide>(a.out + i0 + t) : 0u;
+    r.cpt0 = a.fuse ? (uint32_t)(uint8_t)ld_h<kElide>(a.cpt + i0 + t) : 0u;
+#else
     if (a.fuse) {  // fusion state into L1 now (no registers held), read at List 1
         asm volatile("prefetch.global.L1 [%0];" ::"l"(a.out + i0 + t));
         asm volatile("prefetch.global.L1 [%0];" ::"l"(a.cpt + i0 + t));
     }
+#endif
     load_mix<MC, kElide>(p.cs, r.cpre);
     load_mix<MD, kElide>(p.ds, r.dpre);
     fused_core<MC, MD, kElide>(a, i0, t, p, r, lab);
