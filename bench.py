@@ -527,7 +527,7 @@ def main():
                     help="roofline traffic: ncu child run in this job (N=1), else the stamped "
                          "table if it matches this library build")
     ap.add_argument("--traffic-timeout", type=float, default=600.0)
-    ap.add_argument("--windows", default="near,late,dense,shadow,packed",
+    ap.add_argument("--windows", default="near,late,dense,shadow,packed,l2",
                     help="extra timed windows reported beside the headline ('' = none)")
     ap.add_argument("--child", default=None, help=argparse.SUPPRESS)
     args = ap.parse_args()
@@ -679,6 +679,26 @@ def main():
         windows["dense"] = {**window_value(t), "frames": f"{start + W_}..{start + W_ + K - 1}",
                             "variant": "ldg (reads and writes every state word)"}
         del pd, extd, fr_d
+    if "l2" in wanted and flush is not None:
+        # the same headline frames with the state left in L2 between steps
+        # (a single small stream's 2 x state fits the 126 MB L2): back-to-back
+        # launches, no flush -- how a lone VGA / 1080p camera actually runs
+        pl = make_proc(R, sh, device, args.variant)
+        extl = torch.cuda.ExternalStream(pl.stream_handle, device=dev)
+        preroll(R, pl, sh, range(start - args.preroll, start), device)
+        fr_l = [sh.render(R, start + f, device) for f in range(W_ + K)]
+        torch.cuda.synchronize()
+        barrier()
+        t = timed_window(R, pl, fr_l, W_, K, extl, None)
+        barrier()
+        ksum = allmax(sum(t["kernel_ms"]))
+        windows["l2_resident"] = {**window_value(t),
+                                  "frames": f"{start + W_}..{start + W_ + K - 1}",
+                                  "kernel_ms_per_step": round(ksum / K, 4),
+                                  "state_bytes": int(state_bytes),
+                                  "note": "no L2 flush: back-to-back frames, value from the "
+                                          "event-timed region (launch gaps included)"}
+        del pl, extl, fr_l
     torch.cuda.synchronize()
 
     # ---- e2e: public API, pinned host frames of the sequence in, masks out ---
@@ -687,26 +707,44 @@ def main():
         ring_cap = max(2, (4 << 30) // (5 * npx))
         e2e_steps = min(max(K, 150 if npx < 2**22 else K), ring_cap)
     sync_steps = min(e2e_steps, 5 if npx >= 2**22 else 50)
-    pe = make_proc(R, sh, device, args.variant)
-    preroll(R, pe, sh, range(start - args.preroll, start), device)
-    nhost = e2e_steps + sync_steps
-    host, keep = [], []
-    for f in range(nhost):  # frames start.. of the sequence, each a planar pinned buffer
-        src = sh.render(R, start + f, device)
-        buf = torch.empty(5 * npx, dtype=torch.uint8, pin_memory=True)
-        for idx, k in enumerate(("r", "g", "b")):
-            buf[idx * npx:(idx + 1) * npx].copy_(src[k].reshape(-1))
-        buf[3 * npx:].view(torch.int16).copy_(src["depth"].view(torch.int16).reshape(-1))
-        a = buf.numpy()
-        host.append((a[:npx], a[npx:2 * npx], a[2 * npx:3 * npx],
-                     a[3 * npx:].view(np.uint16)))
-        keep.append(buf)
-        del src
-    outs = [torch.empty(npx, dtype=torch.uint8, pin_memory=True).numpy() for _ in range(2)]
-    torch.cuda.synchronize()
     shp = (sh.streams, sh.h, sh.W) if sh.streams > 1 else (sh.h, sh.W)
-    host = [tuple(x.reshape(shp) for x in hf) for hf in host]
+    nwarm = 3  # untimed host submits (first-call staging set-up), frames start-3..start-1
+
+    def host_ring(frames, packed):
+        """Pinned host buffers of `frames`: planar r|g|b|depth, or R,G,B-
+        interleaved colour + depth (one buffer per frame)."""
+        ring, keep = [], []
+        for f in frames:
+            src = sh.render(R, f, device)
+            buf = torch.empty(5 * npx, dtype=torch.uint8, pin_memory=True)
+            if packed:
+                buf[:3 * npx].copy_(torch.stack([src["r"], src["g"], src["b"]], dim=-1).reshape(-1))
+            else:
+                for idx, k in enumerate(("r", "g", "b")):
+                    buf[idx * npx:(idx + 1) * npx].copy_(src[k].reshape(-1))
+            buf[3 * npx:].view(torch.int16).copy_(src["depth"].view(torch.int16).reshape(-1))
+            a = buf.numpy()
+            dep = a[3 * npx:].view(np.uint16).reshape(shp)
+            if packed:
+                ring.append((a[:3 * npx].reshape(*shp, 3), dep))
+            else:
+                ring.append((a[:npx].reshape(shp), a[npx:2 * npx].reshape(shp),
+                             a[2 * npx:3 * npx].reshape(shp), dep))
+            keep.append(buf)
+            del src
+        torch.cuda.synchronize()
+        return ring, keep
+
+    pe = make_proc(R, sh, device, args.variant)
+    preroll(R, pe, sh, range(start - args.preroll, start - nwarm), device)
+    nhost = e2e_steps + sync_steps
+    host, keep = host_ring(range(start - nwarm, start + nhost), packed=False)
+    warm, host = host[:nwarm], host[nwarm:]
+    outs = [torch.empty(npx, dtype=torch.uint8, pin_memory=True).numpy() for _ in range(2)]
     outs = [o.reshape(shp) for o in outs]
+    for k in range(nwarm):
+        pe.submit(*warm[k], fused=outs[k % 2])
+    pe.sync()
     barrier()
     with ClockSampler(device) as clk_e2e:
         t0 = time.perf_counter()
@@ -759,17 +797,12 @@ def main():
     e2e_packed = None
     if "packed" in wanted:
         pi = make_proc(R, sh, device, args.variant)
-        preroll(R, pi, sh, range(start - args.preroll, start), device)
-        ring, keep = [], []
-        for f in range(e2e_steps):
-            src = sh.render(R, start + f, device)
-            buf = torch.empty(5 * npx, dtype=torch.uint8, pin_memory=True)
-            buf[:3 * npx].copy_(torch.stack([src["r"], src["g"], src["b"]], dim=-1).reshape(-1))
-            buf[3 * npx:].view(torch.int16).copy_(src["depth"].view(torch.int16).reshape(-1))
-            a = buf.numpy()
-            ring.append((a[:3 * npx].reshape(*shp, 3), a[3 * npx:].view(np.uint16).reshape(shp)))
-            keep.append(buf)
-            del src
+        preroll(R, pi, sh, range(start - args.preroll, start - nwarm), device)
+        ring, keep = host_ring(range(start - nwarm, start + e2e_steps), packed=True)
+        for k in range(nwarm):
+            pi.submit_interleaved(*ring[k], order="rgb", fused=outs[k % 2])
+        pi.sync()
+        ring = ring[nwarm:]
         torch.cuda.synchronize()
         barrier()
         t0 = time.perf_counter()

@@ -336,8 +336,11 @@ __global__ void __launch_bounds__(kThreads)
 #ifndef RGBDSEG_PRE_COLOR  // colour components loaded with the flag words (2 or 3)
 #define RGBDSEG_PRE_COLOR 2
 #endif
+#ifndef RGBDSEG_ELIDE_MINB  // resident blocks of the elided K1 (A/B builds override)
+#define RGBDSEG_ELIDE_MINB 12
+#endif
 #ifndef RGBDSEG_FUSED_MIN_BLOCKS
-#define RGBDSEG_FUSED_MIN_BLOCKS(elide) ((elide) ? 12 : 6)
+#define RGBDSEG_FUSED_MIN_BLOCKS(elide) ((elide) ? RGBDSEG_ELIDE_MINB : 6)
 #endif
 // First-round values of one K1 pixel: everything that does not depend on
 // its flag words -- inputs, both flag words, colour components
