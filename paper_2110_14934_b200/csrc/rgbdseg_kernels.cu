@@ -145,6 +145,21 @@ __device__ __forceinline__ void load_mix_need(const float* s, Mixture<N, C>& m, 
     }
 }
 
+// load_mix_need with plain (L1-allocating) loads: the lines were prefetched
+// into L1 earlier (fused_core's flag-aware colour prefetch).
+template <int L, int N, int C>
+__device__ __forceinline__ void load_mix_need_l1(const float* s, Mixture<N, C>& m, uint32_t need,
+                                                 float vvar) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        const bool ld = (need >> i) & 1u;
+#pragma unroll
+        for (int c = 0; c < C; ++c) m.mu[i][c] = ld ? s[(i * C + c) * kBlockPx] : 0.0f;
+        m.var[i] = ld ? s[(L * C + i) * kBlockPx] : vvar;
+        m.w[i] = ld ? s[(L * C + L + i) * kBlockPx] : 0.0f;
+    }
+}
+
 // Dense store (ModelBank::scatter, segmenter.cpp:49-56).
 template <int L, bool H = false, int N, int C>
 __device__ __forceinline__ void store_mix(float* s, const Mixture<N, C>& m) {
@@ -201,7 +216,7 @@ __device__ __forceinline__ uint32_t replay_pixel(float* s, const float (&v)[C], 
     return label;
 }
 
-template <int M, int C, int N, int P, bool kElide, bool kVirt>
+template <int M, int C, int N, int P, bool kElide, bool kVirt, bool kL1 = false>
 __device__ __forceinline__ uint32_t step_pixel_n(float* s, const Mixture<(P > 0 ? P : 1), C>& pre,
                                                  uint32_t need, const float (&v)[C],
                                                  const MixCfg& k, const BankView& bk,
@@ -210,7 +225,10 @@ __device__ __forceinline__ uint32_t step_pixel_n(float* s, const Mixture<(P > 0 
     // components P.. that are touched; with kVirt, N-1 is untouched in every
     // lane (a compile-time zero bit: no load, constant values)
     constexpr uint32_t kLoad = ~((1u << P) - 1u) & (kVirt ? ~(1u << (N - 1)) : ~0u);
-    load_mix_need<M, kElide>(s, m, need & kLoad, bk.vvar);
+    if constexpr (kL1)
+        load_mix_need_l1<M>(s, m, need & kLoad, bk.vvar);
+    else
+        load_mix_need<M, kElide>(s, m, need & kLoad, bk.vvar);
 #pragma unroll
     for (int i = 0; i < (P < N ? P : N); ++i) {  // loaded with the flags (exact values)
 #pragma unroll
@@ -240,7 +258,7 @@ __device__ __forceinline__ uint32_t step_pixel_n(float* s, const Mixture<(P > 0 
 // components where Kw is the warp's largest touched prefix (warp-uniform, so
 // a warp runs one specialisation; the dense variant always takes N = M).
 // Components 0..P-1 arrive in `pre`, loaded before the flags were known.
-template <int M, int C, int P, bool kElide>
+template <int M, int C, int P, bool kElide, bool kL1 = false>
 __device__ __forceinline__ uint32_t k1_bank_pixel(float* s, const Mixture<(P > 0 ? P : 1), C>& pre,
                                                   uint32_t need, int Kw, const float (&v)[C],
                                                   const MixCfg& k, const BankView& bk,
@@ -255,13 +273,13 @@ __device__ __forceinline__ uint32_t k1_bank_pixel(float* s, const Mixture<(P > 0
     // Component N-1 is untouched in every lane whenever Kw < M (kVirt).
     if (!kElide) return step_pixel_n<M, C, M, P, false, false>(s, pre, need, v, k, bk, f, replay);
     const int N = min(Kw + 1, M);
-    if (N <= 2) return step_pixel_n<M, C, 2, P, true, true>(s, pre, need, v, k, bk, f, replay);
+    if (N <= 2) return step_pixel_n<M, C, 2, P, true, true, kL1>(s, pre, need, v, k, bk, f, replay);
     if constexpr (M >= 4)
-        if (N == 3) return step_pixel_n<M, C, 3, P, true, true>(s, pre, need, v, k, bk, f, replay);
+        if (N == 3) return step_pixel_n<M, C, 3, P, true, true, kL1>(s, pre, need, v, k, bk, f, replay);
     if constexpr (M >= 5)
-        if (N == 4) return step_pixel_n<M, C, 4, P, true, true>(s, pre, need, v, k, bk, f, replay);
-    if (Kw == M - 1) return step_pixel_n<M, C, M, P, true, true>(s, pre, need, v, k, bk, f, replay);
-    return step_pixel_n<M, C, M, P, true, false>(s, pre, need, v, k, bk, f, replay);
+        if (N == 4) return step_pixel_n<M, C, 4, P, true, true, kL1>(s, pre, need, v, k, bk, f, replay);
+    if (Kw == M - 1) return step_pixel_n<M, C, M, P, true, true, kL1>(s, pre, need, v, k, bk, f, replay);
+    return step_pixel_n<M, C, M, P, true, false, kL1>(s, pre, need, v, k, bk, f, replay);
 }
 
 // ---------------------------------------------------------------- evaluation
@@ -348,6 +366,12 @@ __global__ void __launch_bounds__(kThreads)
 // initialised pixel, colour component 1 in most; a loaded untouched
 // component equals its substitute).  Only the rest waits for the flags.
 constexpr int kPre = RGBDSEG_PRE_COLOR;
+// 1: once the flags are known, prefetch into L1 the colour planes the
+// second load round will read (components kPre..N-1 this lane needs), so
+// their latency overlaps the depth step; those loads then go through L1.
+#ifndef RGBDSEG_PF_COLOR
+#define RGBDSEG_PF_COLOR 0
+#endif
 // Where K1 reads its fusion state (out, cpt): 0 = at List 1 (prefetched to
 // L1 in round one), 1 = right after the depth step, 2 = in round one.
 #ifndef RGBDSEG_FUSE_LOAD
@@ -409,6 +433,21 @@ __device__ __forceinline__ void fused_core(const FusedArgs& a, size_t i0, unsign
         kd = __reduce_max_sync(am, (r.raw != 0 && (r.df & 0xffu)) ? touched_prefix<MD>(r.df) : 1);
     }
 
+#if RGBDSEG_PF_COLOR
+    if (kElide && (r.cf & 0xffu)) {
+        const int N = min(kc + 1, MC);
+        const uint32_t pf = cneed & ~((1u << kPre) - 1u) & ((1u << N) - 1u);
+#pragma unroll
+        for (int i = kPre; i < MC; ++i)
+            if ((pf >> i) & 1u) {
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(p.cs + (i * 3 + c) * kBlockPx));
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(p.cs + (MC * 3 + i) * kBlockPx));
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(p.cs + (MC * 4 + i) * kBlockPx));
+            }
+    }
+#endif
     // The two banks are independent (only List 1 needs both labels): the
     // small depth step runs first, while the colour components wait in
     // registers.
@@ -434,7 +473,8 @@ __device__ __forceinline__ void fused_core(const FusedArgs& a, size_t i0, unsign
     uint32_t cf1 = r.cf;
     bool replay = false;
     uint32_t lc =
-        k1_bank_pixel<MC, 3, kPre, kElide>(p.cs, cpre, cneed, kc, vc, a.ck, a.color, cf1, replay);
+        k1_bank_pixel<MC, 3, kPre, kElide, kElide && RGBDSEG_PF_COLOR>(p.cs, cpre, cneed, kc, vc,
+                                                                      a.ck, a.color, cf1, replay);
     if (replay) lc = replay_pixel<MC, 3, kElide>(p.cs, vc, a.ck, a.color, cf1);
     if (cf1 != r.cf) st_h<kElide>(p.cflag(), (uint16_t)cf1);
 
