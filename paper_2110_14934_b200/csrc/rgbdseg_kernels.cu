@@ -418,7 +418,15 @@ struct PixAddr {
 // K1 after the first load round: the touched-prefix dispatch, the depth
 // step, the colour step, List 1 and the stores.  Returns the three labels
 // for the evaluation epilogue.
-template <int MC, int MD, bool kElide>
+// kLean: the processor's device-resident fused path -- fusion on, no mask
+// outputs (the launcher checks), so no pointer tests in the epilogue.
+#ifndef RGBDSEG_LEAN  // 1: launch the kLean instantiation when it applies (+0.8%, variants_r02.json)
+#define RGBDSEG_LEAN 1
+#endif
+#ifndef RGBDSEG_FUSE_SEL  // 1: List 1 as selects (fuse_pixel_sel) in K1 (measured 1-2% slower)
+#define RGBDSEG_FUSE_SEL 0
+#endif
+template <int MC, int MD, bool kElide, bool kLean = false>
 __device__ __forceinline__ void fused_core(const FusedArgs& a, size_t i0, unsigned t,
                                            const PixAddr<MC, MD>& p, const Round1& r,
                                            uint32_t (&lab)[3]) {
@@ -479,23 +487,29 @@ __device__ __forceinline__ void fused_core(const FusedArgs& a, size_t i0, unsign
     if (cf1 != r.cf) st_h<kElide>(p.cflag(), (uint16_t)cf1);
 
     // ---- List-1 fusion on the registered depth mask ----
+    const bool fuse = kLean || a.fuse;
 #if RGBDSEG_FUSE_LOAD == 0
-    const uint32_t out0 = a.fuse ? a.out[i0 + t] : 0u;  // L1 hits (plain loads)
-    const int cpt0 = a.fuse ? (int)a.cpt[i0 + t] : 0;
+    const uint32_t out0 = fuse ? a.out[i0 + t] : 0u;  // L1 hits (plain loads)
+    const int cpt0 = fuse ? (int)a.cpt[i0 + t] : 0;
 #elif RGBDSEG_FUSE_LOAD == 2
     const uint32_t out0 = r.out0;
     const int cpt0 = (int)(int8_t)r.cpt0;
 #endif
     uint32_t out = out0;
     int cpt = cpt0;
-    if (a.fuse) {
-        fuse_pixel(lc, ld, a.limit, out, cpt);
+    if (fuse) {
+        if (RGBDSEG_FUSE_SEL)
+            fuse_pixel_sel(lc, ld, a.limit, out, cpt);
+        else
+            fuse_pixel(lc, ld, a.limit, out, cpt);
         if (!kElide || out != out0) st_h<kElide>(a.out + i0 + t, (uint8_t)out);
         if (!kElide || cpt != cpt0) st_h<kElide>(a.cpt + i0 + t, (int8_t)cpt);
     }
-    if (a.rgb_mask) st_h<kElide>(a.rgb_mask + i0 + t, (uint8_t)lc);
-    if (a.depth_mask) st_h<kElide>(a.depth_mask + i0 + t, (uint8_t)ld);
-    if (a.fused_copy) st_h<kElide>(a.fused_copy + i0 + t, (uint8_t)out);
+    if (!kLean) {
+        if (a.rgb_mask) st_h<kElide>(a.rgb_mask + i0 + t, (uint8_t)lc);
+        if (a.depth_mask) st_h<kElide>(a.depth_mask + i0 + t, (uint8_t)ld);
+        if (a.fused_copy) st_h<kElide>(a.fused_copy + i0 + t, (uint8_t)out);
+    }
     lab[0] = lc;
     lab[1] = ld;
     lab[2] = out;
@@ -506,7 +520,7 @@ __device__ __forceinline__ void fused_core(const FusedArgs& a, size_t i0, unsign
 // (a.r, RGB or BGR by a.bgr -- engine.cpp:39-56's aos_to_soa layout, or
 // OpenCV's BGR), deinterleaved here in the first load round: a warp's three
 // byte loads cover the same 96 contiguous bytes the three planar loads would.
-template <int MC, int MD, bool kElide, bool kPacked = false>
+template <int MC, int MD, bool kElide, bool kPacked = false, bool kLean = false>
 __device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i0, unsigned t,
                                             uint32_t (&lab)[3]) {
     const PixAddr<MC, MD> p(a, i0, t);
@@ -529,19 +543,19 @@ __device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i0, unsig
     r.out0 = a.fuse ? ld_h<kElide>(a.out + i0 + t) : 0u;
     r.cpt0 = a.fuse ? (uint32_t)(uint8_t)ld_h<kElide>(a.cpt + i0 + t) : 0u;
 #else
-    if (a.fuse) {  // fusion state into L1 now (no registers held), read at List 1
+    if (kLean || a.fuse) {  // fusion state into L1 now (no registers held), read at List 1
         asm volatile("prefetch.global.L1 [%0];" ::"l"(a.out + i0 + t));
         asm volatile("prefetch.global.L1 [%0];" ::"l"(a.cpt + i0 + t));
     }
 #endif
     load_mix<MC, kElide>(p.cs, r.cpre);
     load_mix<MD, kElide>(p.ds, r.dpre);
-    fused_core<MC, MD, kElide>(a, i0, t, p, r, lab);
+    fused_core<MC, MD, kElide, kLean>(a, i0, t, p, r, lab);
 }
 
 // kEval: with the evaluation epilogue (a.gt set).  A separate instantiation,
 // so the plain kernel's register allocation carries none of it (measured 6%).
-template <int MC, int MD, bool kElide, bool kEval, bool kPacked = false>
+template <int MC, int MD, bool kElide, bool kEval, bool kPacked = false, bool kLean = false>
 __global__ void __launch_bounds__(kThreads, RGBDSEG_FUSED_MIN_BLOCKS(kElide))
     k_fused_ldg(const __grid_constant__ FusedArgs a) {
     const size_t i0 = (size_t)blockIdx.x * kThreads;
@@ -565,7 +579,7 @@ __global__ void __launch_bounds__(kThreads, RGBDSEG_FUSED_MIN_BLOCKS(kElide))
         }
     }
     uint32_t lab[3] = {0u, 0u, 0u};
-    if (active) fused_pixel<MC, MD, kElide, kPacked>(a, i0, threadIdx.x, lab);
+    if (active) fused_pixel<MC, MD, kElide, kPacked, kLean>(a, i0, threadIdx.x, lab);
     if constexpr (kEval) {  // evaluation epilogue: the masks never leave registers
         const uint32_t g = active ? (uint32_t)a.gt[i] : 0u;
         eval_accumulate<3>(active, a.base + i, a.stream_px, lab, g, a.counts);
@@ -1516,6 +1530,8 @@ cudaError_t fused_ldg_md(const FusedArgs& a, bool elide, cudaStream_t s) {
                 k_fused_x2<MC, MD><<<(unsigned)((a.n + 2 * kThreads - 1) / (2 * kThreads)), kThreads, 0, s>>>(a);
             else if constexpr (RGBDSEG_PIPE != 0)
                 k_fused_pipe<MC, MD><<<pipe_blocks<MC, MD>(a.n), kThreads, 0, s>>>(a);
+            else if (RGBDSEG_LEAN && a.fuse && !a.rgb_mask && !a.depth_mask && !a.fused_copy)
+                k_fused_ldg<MC, MD, true, false, false, true><<<nb, kThreads, 0, s>>>(a);
             else
                 k_fused_ldg<MC, MD, true, false><<<nb, kThreads, 0, s>>>(a);
         }

@@ -56,3 +56,15 @@ extern "C" int core_step(Rec* r, const float* v, const Cfg* k) {
     }
     return -1;
 }
+
+// List 1 (fusion.cpp:29-44): the branchy and the select form of one step.
+extern "C" void core_fuse(int sel, unsigned r, unsigned d, int limit, unsigned* out, int* cpt) {
+    uint32_t o = *out;
+    int c = *cpt;
+    if (sel)
+        fuse_pixel_sel(r, d, limit, o, c);
+    else
+        fuse_pixel(r, d, limit, o, c);
+    *out = o;
+    *cpt = c;
+}

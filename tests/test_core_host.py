@@ -112,3 +112,36 @@ def test_core_non_finite_states(core, port, bad):
         x = np.frombuffer(bytes(mc), np.float32)[2:]
         y = np.frombuffer(bytes(m), np.float32)[2:]
         assert np.array_equal(x, y, equal_nan=True), (bad, trial)
+
+
+def test_fuse_select_form_equals_list1(core, port):
+    """fuse_pixel_sel (K1's branch-free List 1) == fuse_pixel == the oracle's
+    fuse step for every (r, d, out, cpt) and counter limits incl. 0 and
+    negatives (fusion.cpp:29-44)."""
+    f = core.core_fuse
+    f.argtypes = [C.c_int, C.c_uint, C.c_uint, C.c_int, C.POINTER(C.c_uint), C.POINTER(C.c_int)]
+    for limit in list(range(-3, 8)) + [100, 127, 128, 200]:
+        for r in (0, 1):
+            for d in (0, 1):
+                for out in (0, 1):
+                    for cpt in range(-128, 128):
+                        res = []
+                        for sel in (0, 1):
+                            o, c = C.c_uint(out), C.c_int(cpt)
+                            f(sel, r, d, limit, C.byref(o), C.byref(c))
+                            res.append((o.value, c.value))
+                        assert res[0] == res[1], (limit, r, d, out, cpt, res)
+    # and against the oracle's List 1 (orc_fuse) on a plane of random states
+    rng = np.random.default_rng(5)
+    n = 4096
+    for limit in (1, 3, 100):
+        out = rng.integers(0, 2, n).astype(np.uint8)
+        cpt = rng.integers(-limit, limit + 1, n).astype(np.int8)
+        rgb = rng.integers(0, 2, n).astype(np.uint8)
+        dep = rng.integers(0, 2, n).astype(np.uint8)
+        o2, c2 = out.copy(), cpt.copy()
+        port.lib.orc_fuse(o2, c2, n, limit, rgb, dep)
+        for i in range(n):
+            o, c = C.c_uint(int(out[i])), C.c_int(int(cpt[i]))
+            f(1, int(rgb[i]), int(dep[i]), limit, C.byref(o), C.byref(c))
+            assert (o.value, c.value) == (int(o2[i]), int(c2[i])), (limit, i)
