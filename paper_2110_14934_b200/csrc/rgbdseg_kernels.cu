@@ -520,6 +520,9 @@ __device__ __forceinline__ void fused_core(const FusedArgs& a, size_t i0, unsign
 // (a.r, RGB or BGR by a.bgr -- engine.cpp:39-56's aos_to_soa layout, or
 // OpenCV's BGR), deinterleaved here in the first load round: a warp's three
 // byte loads cover the same 96 contiguous bytes the three planar loads would.
+#ifndef RGBDSEG_R1_DEPTH_FIRST  // 1: issue the depth component before the colour ones
+#define RGBDSEG_R1_DEPTH_FIRST 0
+#endif
 template <int MC, int MD, bool kElide, bool kPacked = false, bool kLean = false>
 __device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i0, unsigned t,
                                             uint32_t (&lab)[3]) {
@@ -548,8 +551,13 @@ __device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i0, unsig
         asm volatile("prefetch.global.L1 [%0];" ::"l"(a.cpt + i0 + t));
     }
 #endif
+#if RGBDSEG_R1_DEPTH_FIRST  // the depth step runs first: its words first
+    load_mix<MD, kElide>(p.ds, r.dpre);
+    load_mix<MC, kElide>(p.cs, r.cpre);
+#else
     load_mix<MC, kElide>(p.cs, r.cpre);
     load_mix<MD, kElide>(p.ds, r.dpre);
+#endif
     fused_core<MC, MD, kElide, kLean>(a, i0, t, p, r, lab);
 }
 
