@@ -16,7 +16,7 @@ all: lib oracle
 
 lib: $(LIB)
 
-$(CSRC)/%.o: $(CSRC)/%.cu $(CSRC)/gmm_pixel.cuh $(CSRC)/rgbdseg_kernels.cuh include/rgbdseg_c.h
+$(CSRC)/%.o: $(CSRC)/%.cu $(CSRC)/gmm_pixel.cuh $(CSRC)/rgbdseg_kernels.cuh $(CSRC)/k1_experiments.cuh include/rgbdseg_c.h
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
 # cudart is linked shared (libcudart.so.12, the process's one CUDA runtime).
