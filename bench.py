@@ -381,9 +381,21 @@ def measure_traffic(args, npx: int):
     cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
            "--clock-control", "none", "-k", "regex:k_fused", "-s", str(skip), "-c",
            str(args.steps), "--csv", "--log-file", log, *child]
+    # the child is ONE process on this rank's GPU, never a member of the job
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "LOCAL_WORLD_SIZE", "GROUP_RANK",
+                        "ROLE_RANK", "MASTER_ADDR", "MASTER_PORT", "TORCHELASTIC_RUN_ID")}
+    try:
+        import torch
+
+        env["CUDA_VISIBLE_DEVICES"] = str(torch.cuda.current_device()) \
+            if "CUDA_VISIBLE_DEVICES" not in os.environ else \
+            os.environ["CUDA_VISIBLE_DEVICES"].split(",")[torch.cuda.current_device()]
+    except Exception:  # noqa: BLE001
+        pass
     try:
         r = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True,
-                           timeout=args.traffic_timeout)
+                           timeout=args.traffic_timeout, env=env)
         ls = parse_ncu_csv(open(log).read())
         if r.returncode != 0 or len(ls) != args.steps:
             return None, f"ncu rc={r.returncode}, {len(ls)} launches: {r.stdout[-300:]!r}"
