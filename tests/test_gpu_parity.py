@@ -1469,3 +1469,48 @@ def test_config5_8k_full_frames_row_tiles_vs_reference(R, cuda):
         del r, g, b, d
     torch.cuda.synchronize()
     _check_banks_vs_ref(ref, rp, [(p.color_bank(), p.depth_bank()) for p in procs], w * h, M)
+
+
+@pytest.mark.parametrize("variant", ["auto", "ldg"])
+def test_device_frames_without_outputs_lean_path(R, port, cuda, variant):
+    """Device-resident frames processed with NO mask outputs launch K1's
+    fused-mask-only instantiation (kLean; the bench's `value` path).  Across
+    scenario A's illumination step, with depth holes and a partial last
+    block, its fusion state (out = the fused mask, cpt), bank words and flags
+    equal the oracle's every frame, and equal a second processor fed the
+    same frames WITH a fused output (the mask-writing instantiation)."""
+    import torch
+
+    w, h, S, M = 53, 41, 2, 5
+    cfg = R.RunConfig.defaults()
+    cfg.color_gmm.components = cfg.depth_gmm.components = M
+    lean = R.SequenceProcessor(w, h, cfg, streams=S, variant=variant)
+    full = R.SequenceProcessor(w, h, cfg, streams=S, variant=variant)
+    orc = [O.PortProcessor(port, w * h, O.color_cfg(M), O.depth_cfg(M)) for _ in range(S)]
+    scenes = [O.PortScene(port, "A", w, h, seed=s + 3) for s in range(S)]
+    n = S * w * h
+    for f in range(90, 130):
+        frs = [sc.render(f) for sc in scenes]
+        host = {k: np.stack([getattr(fr, k) for fr in frs]) for k in ("r", "g", "b")}
+        host["depth"] = np.stack([holes(fr.depth, f) for fr in frs])
+        dev = {k: torch.from_numpy(v.view(np.int16) if v.dtype == np.uint16 else v)
+               .to(cuda).view(torch.uint16 if v.dtype == np.uint16 else torch.uint8)
+               for k, v in host.items()}
+        torch.cuda.synchronize()
+        lean.process(dev["r"], dev["g"], dev["b"], dev["depth"], want=())
+        fused = torch.empty(n, dtype=torch.uint8, device=cuda)
+        full.process(dev["r"], dev["g"], dev["b"], dev["depth"], want=(), out={"fused": fused})
+        got = lean.fusion_state().out.reshape(S, -1)
+        ref = fused.cpu().numpy().reshape(S, -1)
+        for s in range(S):
+            _, _, fu = orc[s].process(host["r"][s], host["g"][s], host["b"][s], host["depth"][s])
+            assert np.array_equal(got[s], fu), (f, s)
+            assert np.array_equal(ref[s], fu), (f, s)
+    assert np.array_equal(lean.fusion_state().cpt, full.fusion_state().cpt)
+    for bank in ("color_bank", "depth_bank"):
+        P = getattr(lean, bank)().planes().reshape(-1, S, w * h)
+        Q = getattr(full, bank)().planes().reshape(-1, S, w * h)
+        assert P.tobytes() == Q.tobytes(), bank
+        for s in range(S):
+            o = orc[s].color if bank == "color_bank" else orc[s].depth
+            assert P[:, s].tobytes() == o.planes().tobytes(), (bank, s)
