@@ -303,6 +303,7 @@ int rgbdseg_init_mixtures(const float* values, int channels, size_t n,
     if (channels < 1 || channels > 4)
         return fail(RGBDSEG_EINVAL, "init_mixture: bad observation dimensionality");
     if (n == 0) return RGBDSEG_OK;
+    if (!values || !out) return fail(RGBDSEG_EINVAL, "init_mixture: null buffer");
     GUARD(device);
     float* dv;
     PixRec* dr;
@@ -327,6 +328,7 @@ int rgbdseg_step_mixtures(rgbdseg_pixel_mixture* mix, const float* values, int c
     if (channels < 1 || channels > 4)
         return fail(RGBDSEG_EINVAL, "step_pixel: bad observation dimensionality");
     if (n == 0) return RGBDSEG_OK;
+    if (!mix || !values) return fail(RGBDSEG_EINVAL, "step_pixel: null buffer");
     // Shapes are checked before anything runs, so a rejected call leaves
     // every record untouched (the kernel's 255 label stays a backstop).
     {
@@ -393,6 +395,10 @@ static int mix_op(int op, rgbdseg_pixel_mixture* mix, const float* values, int c
                   int device, const char* who) {
     if (!cfg) return fail(RGBDSEG_EINVAL, std::string(who) + ": null config");
     if (n == 0) return RGBDSEG_OK;
+    if (!mix || !matched || (op != kOpClassify && !values) || (op == kOpClassify && !labels))
+        return fail(RGBDSEG_EINVAL, std::string(who) + ": null buffer");
+    if (op != kOpClassify && (channels < 1 || channels > 4))
+        return fail(RGBDSEG_EINVAL, std::string(who) + ": bad observation dimensionality");
     GUARD(device);
     std::vector<rgbdseg_pixel_mixture> hm;
     const rgbdseg_pixel_mixture* recs = mix;

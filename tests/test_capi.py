@@ -152,3 +152,34 @@ def test_aos_soa_helpers_match_reference_layout():
         R.aos_to_soa(np.zeros((4, 4), np.uint8))
     with pytest.raises(ValueError, match="soa_to_aos: dimension mismatch"):
         R.soa_to_aos(r, g, np.zeros((3, 3), np.uint8))
+
+
+def test_per_pixel_entry_points_reject_null_buffers_before_touching_a_gpu():
+    """init/step/match/classify/update over n > 0 records with a null buffer
+    return EINVAL (never dereference it), before any CUDA call."""
+    import ctypes as C
+
+    from paper_2110_14934_b200 import _lib
+
+    lib = _lib.lib
+    cfg = _lib.MixtureCfg()
+    lib.rgbdseg_mixture_defaults(C.byref(cfg))
+    rec = (_lib.PixelMixtureRec * 2)()
+    vals = (C.c_float * 6)()
+    lab = (C.c_uint8 * 2)()
+    mt = (C.c_int32 * 2)()
+    calls = [
+        ("init_mixture", lambda: lib.rgbdseg_init_mixtures(None, 3, 2, C.byref(cfg), rec, 0)),
+        ("init_mixture", lambda: lib.rgbdseg_init_mixtures(vals, 3, 2, C.byref(cfg), None, 0)),
+        ("step_pixel", lambda: lib.rgbdseg_step_mixtures(None, vals, 3, 2, C.byref(cfg), lab, 0)),
+        ("step_pixel", lambda: lib.rgbdseg_step_mixtures(rec, None, 3, 2, C.byref(cfg), lab, 0)),
+        ("match_component", lambda: lib.rgbdseg_match_components(rec, vals, 3, 2, C.byref(cfg),
+                                                                 None, 0)),
+        ("classify", lambda: lib.rgbdseg_classify_mixtures(rec, mt, 2, C.byref(cfg), None, 0)),
+        ("update_mixture", lambda: lib.rgbdseg_update_mixtures(rec, None, 3, 2, mt, C.byref(cfg),
+                                                               0)),
+    ]
+    for who, call in calls:
+        assert call() == _lib.EINVAL, who
+        msg = lib.rgbdseg_last_error().decode()
+        assert "null buffer" in msg, (who, msg)
