@@ -165,6 +165,7 @@ struct Scratch {
 // Stage `bytes` of a host-or-device source into device memory: device
 // pointers are used in place, host pointers are copied into `scratch`.
 int stage_in(const void* src, size_t bytes, Scratch& scratch, const void** dev, cudaStream_t s) {
+    if (!src) return fail(RGBDSEG_EINVAL, "null input plane");
     if (on_device(src)) {
         *dev = src;
         return RGBDSEG_OK;
@@ -517,10 +518,11 @@ void rgbdseg_bank_destroy(rgbdseg_bank* b) {
     delete b;
 }
 
-int rgbdseg_bank_planes(const rgbdseg_bank* b) { return b->M * b->C + 2 * b->M; }
+int rgbdseg_bank_planes(const rgbdseg_bank* b) { return b ? b->M * b->C + 2 * b->M : 0; }
 
 int rgbdseg_bank_device_ptrs(const rgbdseg_bank* b, void** tiles, size_t* block_bytes,
                              size_t* nblocks) {
+    if (!b) return fail(RGBDSEG_EINVAL, "bank_device_ptrs: null handle");
     if (tiles) *tiles = b->state;
     if (block_bytes) *block_bytes = (size_t)bank_stride(b->M, b->C) * sizeof(float);
     if (nblocks) *nblocks = b->nblocks;
@@ -551,12 +553,14 @@ static int bank_xfer(rgbdseg_bank* b, int plane, void* dst, const void* src) {
 }
 
 int rgbdseg_bank_download(const rgbdseg_bank* b, int plane, void* dst) {
+    if (!b) return fail(RGBDSEG_EINVAL, "bank_download: null handle");
     GUARD(b->device);
     if (int rc = drain_owner(b->owner)) return rc;
     return bank_xfer(const_cast<rgbdseg_bank*>(b), plane, dst, nullptr);
 }
 
 int rgbdseg_bank_upload(rgbdseg_bank* b, int plane, const void* src) {
+    if (!b) return fail(RGBDSEG_EINVAL, "bank_upload: null handle");
     GUARD(b->device);
     if (int rc = drain_owner(b->owner)) return rc;
     return bank_xfer(b, plane, nullptr, src);
@@ -585,6 +589,7 @@ static int finish_mask(uint8_t* dev_mask, uint8_t* mask_out, size_t n, cudaStrea
 
 int rgbdseg_segment_color(rgbdseg_bank* b, const uint8_t* r, const uint8_t* g, const uint8_t* bl,
                           const rgbdseg_mixture_cfg* cfg, uint8_t* mask_out) {
+    if (!b) return fail(RGBDSEG_EINVAL, "segment_color: null handle");
     if (int rc = bank_call_checks(b, cfg, RGBDSEG_COLOR3, "segment_color")) return rc;
     GUARD(b->device);
     if (int rc = drain_owner(b->owner)) return rc;
@@ -609,6 +614,7 @@ int rgbdseg_segment_color(rgbdseg_bank* b, const uint8_t* r, const uint8_t* g, c
 
 int rgbdseg_segment_depth(rgbdseg_bank* b, const uint16_t* depth_mm,
                           const rgbdseg_mixture_cfg* cfg, uint8_t* mask_out) {
+    if (!b) return fail(RGBDSEG_EINVAL, "segment_depth: null handle");
     if (int rc = bank_call_checks(b, cfg, RGBDSEG_DEPTH1, "segment_depth")) return rc;
     GUARD(b->device);
     if (int rc = drain_owner(b->owner)) return rc;
@@ -631,6 +637,7 @@ int rgbdseg_segment_depth(rgbdseg_bank* b, const uint16_t* depth_mm,
 int rgbdseg_segment_augmented(rgbdseg_bank* b, const uint8_t* r, const uint8_t* g,
                               const uint8_t* bl, const uint16_t* depth_mm, float min_mm,
                               float max_mm, const rgbdseg_mixture_cfg* cfg, uint8_t* mask_out) {
+    if (!b) return fail(RGBDSEG_EINVAL, "segment_augmented: null handle");
     if (int rc = bank_call_checks(b, cfg, RGBDSEG_AUGMENTED4, "segment_augmented")) return rc;
     if (!(max_mm > min_mm)) return fail(RGBDSEG_EINVAL, "config: augmented depth range is empty");
     GUARD(b->device);
@@ -700,6 +707,7 @@ void rgbdseg_fusion_destroy(rgbdseg_fusion* f) {
 
 int rgbdseg_fusion_step(rgbdseg_fusion* f, const uint8_t* rgb_mask, const uint8_t* depth_mask,
                         uint8_t* out_copy) {
+    if (!f) return fail(RGBDSEG_EINVAL, "fusion_step: null handle");
     GUARD(f->device);
     if (int rc = drain_owner(f->owner)) return rc;
     const void *dr, *dd;
@@ -714,6 +722,7 @@ int rgbdseg_fusion_step(rgbdseg_fusion* f, const uint8_t* rgb_mask, const uint8_
 }
 
 int rgbdseg_fusion_download(const rgbdseg_fusion* f, uint8_t* out, int8_t* cpt) {
+    if (!f) return fail(RGBDSEG_EINVAL, "fusion_download: null handle");
     GUARD(f->device);
     if (int rc = drain_owner(f->owner)) return rc;
     CU(cudaStreamSynchronize(f->stream));
@@ -723,6 +732,7 @@ int rgbdseg_fusion_download(const rgbdseg_fusion* f, uint8_t* out, int8_t* cpt) 
 }
 
 int rgbdseg_fusion_set_counter_limit(rgbdseg_fusion* f, int counter_limit) {
+    if (!f) return fail(RGBDSEG_EINVAL, "fusion_set_counter_limit: null handle");
     GUARD(f->device);
     if (int rc = drain_owner(f->owner)) return rc;
     CU(cudaStreamSynchronize(f->stream));
@@ -731,6 +741,7 @@ int rgbdseg_fusion_set_counter_limit(rgbdseg_fusion* f, int counter_limit) {
 }
 
 int rgbdseg_fusion_upload(rgbdseg_fusion* f, const uint8_t* out, const int8_t* cpt) {
+    if (!f) return fail(RGBDSEG_EINVAL, "fusion_upload: null handle");
     GUARD(f->device);
     if (int rc = drain_owner(f->owner)) return rc;
     CU(cudaStreamSynchronize(f->stream));
@@ -1208,6 +1219,7 @@ static int submit_impl(rgbdseg_processor* p, const uint8_t* r, const uint8_t* g,
 int rgbdseg_processor_submit(rgbdseg_processor* p, const uint8_t* r, const uint8_t* g,
                              const uint8_t* b, const uint16_t* depth, uint8_t* fused_out,
                              uint8_t* rgb_out, uint8_t* depth_out) {
+    if (!p) return fail(RGBDSEG_EINVAL, "processor_submit: null handle");
     GUARD(p->cfg.device);
     return submit_impl(p, r, g, b, depth, fused_out, rgb_out, depth_out, nullptr, nullptr);
 }
@@ -1215,6 +1227,7 @@ int rgbdseg_processor_submit(rgbdseg_processor* p, const uint8_t* r, const uint8
 int rgbdseg_processor_submit_interleaved(rgbdseg_processor* p, const uint8_t* rgb, int order,
                                          const uint16_t* depth, uint8_t* fused_out,
                                          uint8_t* rgb_out, uint8_t* depth_out) {
+    if (!p) return fail(RGBDSEG_EINVAL, "processor_submit_interleaved: null handle");
     GUARD(p->cfg.device);
     if (order != RGBDSEG_ORDER_RGB && order != RGBDSEG_ORDER_BGR)
         return fail(RGBDSEG_EINVAL, "process: unknown channel order");
@@ -1225,6 +1238,7 @@ int rgbdseg_processor_submit_interleaved(rgbdseg_processor* p, const uint8_t* rg
 int rgbdseg_processor_process_interleaved(rgbdseg_processor* p, const uint8_t* rgb, int order,
                                           const uint16_t* depth, uint8_t* fused_out,
                                           uint8_t* rgb_out, uint8_t* depth_out) {
+    if (!p) return fail(RGBDSEG_EINVAL, "processor_process_interleaved: null handle");
     if (int rc = rgbdseg_processor_submit_interleaved(p, rgb, order, depth, fused_out, rgb_out,
                                                       depth_out))
         return rc;
@@ -1235,6 +1249,7 @@ int rgbdseg_processor_submit_eval(rgbdseg_processor* p, const uint8_t* r, const 
                                   const uint8_t* b, const uint16_t* depth, const uint8_t* gt,
                                   int64_t* counts, uint8_t* fused_out, uint8_t* rgb_out,
                                   uint8_t* depth_out) {
+    if (!p) return fail(RGBDSEG_EINVAL, "processor_submit_eval: null handle");
     GUARD(p->cfg.device);
     return submit_impl(p, r, g, b, depth, fused_out, rgb_out, depth_out, gt, counts);
 }
@@ -1243,6 +1258,7 @@ int rgbdseg_processor_process_eval(rgbdseg_processor* p, const uint8_t* r, const
                                    const uint8_t* b, const uint16_t* depth, const uint8_t* gt,
                                    int64_t* counts, uint8_t* fused_out, uint8_t* rgb_out,
                                    uint8_t* depth_out) {
+    if (!p) return fail(RGBDSEG_EINVAL, "processor_process_eval: null handle");
     if (int rc = rgbdseg_processor_submit_eval(p, r, g, b, depth, gt, counts, fused_out, rgb_out,
                                                depth_out))
         return rc;
@@ -1271,6 +1287,7 @@ int rgbdseg_confusion_counts(const uint8_t* pred, const uint8_t* gt, size_t npx,
 }
 
 int rgbdseg_processor_sync(rgbdseg_processor* p) {
+    if (!p) return fail(RGBDSEG_EINVAL, "processor_sync: null handle");
     GUARD(p->cfg.device);
     if (int rc = flush_emit(p)) return rc;
     CU(cudaStreamSynchronize(p->cs[0]));
@@ -1281,6 +1298,7 @@ int rgbdseg_processor_sync(rgbdseg_processor* p) {
 int rgbdseg_processor_process(rgbdseg_processor* p, const uint8_t* r, const uint8_t* g,
                               const uint8_t* b, const uint16_t* depth, uint8_t* fused_out,
                               uint8_t* rgb_out, uint8_t* depth_out) {
+    if (!p) return fail(RGBDSEG_EINVAL, "processor_process: null handle");
     if (int rc = rgbdseg_processor_submit(p, r, g, b, depth, fused_out, rgb_out, depth_out))
         return rc;
     return rgbdseg_processor_sync(p);
@@ -1291,6 +1309,7 @@ int64_t rgbdseg_processor_frames(const rgbdseg_processor* p) { return p->frames;
 // Stream ordering with a caller's CUDA stream (the library's streams are
 // non-blocking, so they are not ordered with the legacy default stream).
 int rgbdseg_processor_wait_stream(rgbdseg_processor* p, void* stream) {
+    if (!p) return fail(RGBDSEG_EINVAL, "processor_wait_stream: null handle");
     GUARD(p->cfg.device);
     CU(cudaEventRecord(p->ev_user, (cudaStream_t)stream));
     CU(cudaStreamWaitEvent(p->cs[0], p->ev_user, 0));
@@ -1299,6 +1318,7 @@ int rgbdseg_processor_wait_stream(rgbdseg_processor* p, void* stream) {
 }
 
 int rgbdseg_processor_signal_stream(rgbdseg_processor* p, void* stream) {
+    if (!p) return fail(RGBDSEG_EINVAL, "processor_signal_stream: null handle");
     GUARD(p->cfg.device);
     for (int i = 0; i < 2; ++i) {
         CU(cudaEventRecord(p->ev_done[i], p->cs[i]));
@@ -1306,12 +1326,13 @@ int rgbdseg_processor_signal_stream(rgbdseg_processor* p, void* stream) {
     }
     return RGBDSEG_OK;
 }
-rgbdseg_bank* rgbdseg_processor_color_bank(rgbdseg_processor* p) { return p->color; }
-rgbdseg_bank* rgbdseg_processor_depth_bank(rgbdseg_processor* p) { return p->depth; }
-rgbdseg_fusion* rgbdseg_processor_fusion(rgbdseg_processor* p) { return p->fusion; }
-void* rgbdseg_processor_stream(rgbdseg_processor* p) { return (void*)p->cs[0]; }
+rgbdseg_bank* rgbdseg_processor_color_bank(rgbdseg_processor* p) { return p ? p->color : nullptr; }
+rgbdseg_bank* rgbdseg_processor_depth_bank(rgbdseg_processor* p) { return p ? p->depth : nullptr; }
+rgbdseg_fusion* rgbdseg_processor_fusion(rgbdseg_processor* p) { return p ? p->fusion : nullptr; }
+void* rgbdseg_processor_stream(rgbdseg_processor* p) { return p ? (void*)p->cs[0] : nullptr; }
 
 int rgbdseg_processor_set_near_threshold(rgbdseg_processor* p, float rel) {
+    if (!p) return fail(RGBDSEG_EINVAL, "processor_set_near_threshold: null handle");
     GUARD(p->cfg.device);
     if (int rc = rgbdseg_processor_sync(p)) return rc;
     if (!(rel >= 0.0f)) return fail(RGBDSEG_EINVAL, "near-threshold: rel must be >= 0");
@@ -1327,6 +1348,7 @@ int rgbdseg_processor_set_near_threshold(rgbdseg_processor* p, float rel) {
 
 int rgbdseg_processor_near_threshold_counts(rgbdseg_processor* p, uint64_t* color,
                                             uint64_t* depth, uint64_t* pixel_frames) {
+    if (!p) return fail(RGBDSEG_EINVAL, "processor_near_threshold_counts: null handle");
     GUARD(p->cfg.device);
     if (int rc = rgbdseg_processor_sync(p)) return rc;
     unsigned long long h[2] = {0, 0};
@@ -1338,6 +1360,7 @@ int rgbdseg_processor_near_threshold_counts(rgbdseg_processor* p, uint64_t* colo
 }
 
 int rgbdseg_processor_set_variant(rgbdseg_processor* p, int variant) {
+    if (!p) return fail(RGBDSEG_EINVAL, "processor_set_variant: null handle");
     if (variant < kAuto || variant > kLdgElide) return fail(RGBDSEG_EINVAL, "unknown kernel variant");
     p->variant = variant;
     return RGBDSEG_OK;
@@ -1431,6 +1454,7 @@ int rgbdseg_render_scenario(char name, int width, int height, int streams, uint6
 int rgbdseg_render_frame(const rgbdseg_scene_frame* f, uint8_t* r, uint8_t* g, uint8_t* b,
                          uint16_t* depth, uint8_t* gt, int device, void* stream) {
     static_assert(sizeof(SceneFrame) == sizeof(rgbdseg_scene_frame), "scene frame layout");
+    if (!f) return fail(RGBDSEG_EINVAL, "render_frame: null frame");
     if (int rc = check_dims(f->width, f->height, f->streams)) return rc;
     if (f->n_obj < 0 || f->n_obj > 4 || f->n_shadow < 0 || f->n_shadow > 16 || f->n_flicker < 0 ||
         f->n_flicker > 16)

@@ -183,3 +183,31 @@ def test_per_pixel_entry_points_reject_null_buffers_before_touching_a_gpu():
         assert call() == _lib.EINVAL, who
         msg = lib.rgbdseg_last_error().decode()
         assert "null buffer" in msg, (who, msg)
+
+
+def test_null_handles_and_planes_rejected_before_touching_a_gpu():
+    """Every handle-taking entry point returns EINVAL on a null handle (the
+    reference's methods cannot be called on no object; a C caller can)."""
+    import ctypes as C
+
+    from paper_2110_14934_b200 import _lib
+
+    lib = _lib.lib
+    buf = (C.c_uint8 * 16)()
+    calls = {
+        "bank_download": lambda: lib.rgbdseg_bank_download(None, 0, buf),
+        "bank_upload": lambda: lib.rgbdseg_bank_upload(None, 0, buf),
+        "fusion_step": lambda: lib.rgbdseg_fusion_step(None, buf, buf, None),
+        "fusion_download": lambda: lib.rgbdseg_fusion_download(None, buf, None),
+        "fusion_upload": lambda: lib.rgbdseg_fusion_upload(None, buf, None),
+        "processor_process": lambda: lib.rgbdseg_processor_process(None, buf, buf, buf, buf,
+                                                                   None, None, None),
+        "processor_submit": lambda: lib.rgbdseg_processor_submit(None, buf, buf, buf, buf,
+                                                                 None, None, None),
+        "processor_sync": lambda: lib.rgbdseg_processor_sync(None),
+    }
+    for who, call in calls.items():
+        assert call() == _lib.EINVAL, who
+        assert "null handle" in lib.rgbdseg_last_error().decode(), who
+    assert lib.rgbdseg_processor_color_bank(None) is None
+    assert lib.rgbdseg_bank_planes(None) == 0
