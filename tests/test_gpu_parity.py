@@ -1514,3 +1514,65 @@ def test_device_frames_without_outputs_lean_path(R, port, cuda, variant):
         for s in range(S):
             o = orc[s].color if bank == "color_bank" else orc[s].depth
             assert P[:, s].tobytes() == o.planes().tobytes(), (bank, s)
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_fused_processor_random_configs_vs_oracle(R, port, cuda, seed):
+    """K1 under random MixtureConfigs (rates, lambda, T, sigma0 -- which sets
+    the untouched component's folded sigma/band constants --, initial weight,
+    variance floor, component counts, counter limit): fused masks every frame
+    and final banks, flags and fusion state bit-identical to the oracle, for
+    host frames and for device frames on the fused-mask-only path."""
+    import torch
+
+    rng = np.random.default_rng(100 + seed)
+    w, h, S = 44, 28, 2
+
+    def rand_cfg(depth):
+        return dict(components=int(rng.integers(3, 6)),
+                    learning_rate=float(rng.choice([rng.uniform(1e-3, 0.02), rng.uniform(0.02, 0.5)])),
+                    match_lambda=float(rng.uniform(1.5, 4.0)),
+                    background_threshold=float(rng.uniform(0.3, 0.95)),
+                    initial_sigma=float(rng.uniform(10, 400) if depth else rng.uniform(3, 60)),
+                    initial_weight=float(rng.uniform(0.01, 0.3)),
+                    variance_floor=float(rng.uniform(0.5, 20.0)))
+
+    kc, kd = rand_cfg(False), rand_cfg(True)
+    limit = int(rng.integers(1, 6))
+    cfg = R.RunConfig.defaults()
+    for k, v in kc.items():
+        setattr(cfg.color_gmm, k, v)
+    for k, v in kd.items():
+        setattr(cfg.depth_gmm, k, v)
+    cfg.fusion_counter_limit = limit
+    host = R.SequenceProcessor(w, h, cfg, streams=S)
+    dev = R.SequenceProcessor(w, h, cfg, streams=S)
+    oc = O.color_cfg(kc.pop("components"), **kc)
+    od = O.depth_cfg(kd.pop("components"), **kd)
+    orc = [O.PortProcessor(port, w * h, oc, od, limit=limit) for _ in range(S)]
+    scenes = [O.PortScene(port, "AB"[(seed + s) % 2], w, h, seed=seed * 7 + s) for s in range(S)]
+    start = int(rng.integers(0, 200))
+    for f in range(start, start + 50):
+        frs = [sc.render(f) for sc in scenes]
+        r, g, b = (np.stack([getattr(fr, k) for fr in frs]) for k in ("r", "g", "b"))
+        d = np.stack([holes(fr.depth, f) for fr in frs])
+        fm = host.process(r, g, b, d, want=("fused",))
+        td = [torch.from_numpy(np.ascontiguousarray(x)).to(cuda) for x in (r, g, b)]
+        tdd = torch.from_numpy(d.view(np.int16)).to(cuda).view(torch.uint16)
+        torch.cuda.synchronize()
+        dev.process(*td, tdd, want=())
+        got = dev.fusion_state().out.reshape(S, -1)
+        for s in range(S):
+            _, _, fu = orc[s].process(r[s], g[s], b[s], d[s])
+            assert np.array_equal(fm.fused[s].ravel(), fu), (seed, f, s)
+            assert np.array_equal(got[s], fu), (seed, f, s)
+    for p in (host, dev):
+        C = p.color_bank().planes().reshape(-1, S, w * h)
+        D = p.depth_bank().planes().reshape(-1, S, w * h)
+        Fc = p.color_bank().initialized_plane().reshape(S, -1)
+        for s in range(S):
+            assert C[:, s].tobytes() == orc[s].color.planes().tobytes(), (seed, s)
+            assert D[:, s].tobytes() == orc[s].depth.planes().tobytes(), (seed, s)
+            assert np.array_equal(Fc[s], orc[s].color.flags), (seed, s)
+        assert np.array_equal(p.fusion_state().cpt.reshape(S, -1),
+                              np.stack([o.cpt for o in orc])), seed
