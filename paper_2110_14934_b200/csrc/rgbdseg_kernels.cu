@@ -373,7 +373,8 @@ constexpr int kPre = RGBDSEG_PRE_COLOR;
 #define RGBDSEG_PF_COLOR 0
 #endif
 // Where K1 reads its fusion state (out, cpt): 0 = at List 1 (prefetched to
-// L1 in round one), 1 = right after the depth step, 2 = in round one.
+// L1 in round one), 1 = right after the depth step, 2 = in round one,
+// 3 = at List 1 from L2 (prefetched to L2 in round one).
 #ifndef RGBDSEG_FUSE_LOAD
 #define RGBDSEG_FUSE_LOAD 0
 #endif
@@ -472,8 +473,8 @@ __device__ __forceinline__ void fused_core(const FusedArgs& a, size_t i0, unsign
     }
 
 #if RGBDSEG_FUSE_LOAD == 1
-    const uint32_t out0 = a.fuse ? a.out[i0 + t] : 0u;
-    const int cpt0 = a.fuse ? (int)a.cpt[i0 + t] : 0;
+    const uint32_t out0 = (kLean || a.fuse) ? a.out[i0 + t] : 0u;
+    const int cpt0 = (kLean || a.fuse) ? (int)a.cpt[i0 + t] : 0;
 #endif
     // ---- colour stream (segment_color) ----
     const float vc[3] = {r.vc[0], r.vc[1], r.vc[2]};
@@ -491,6 +492,9 @@ __device__ __forceinline__ void fused_core(const FusedArgs& a, size_t i0, unsign
 #if RGBDSEG_FUSE_LOAD == 0
     const uint32_t out0 = fuse ? a.out[i0 + t] : 0u;  // L1 hits (plain loads)
     const int cpt0 = fuse ? (int)a.cpt[i0 + t] : 0;
+#elif RGBDSEG_FUSE_LOAD == 3
+    const uint32_t out0 = fuse ? ld_h<true>(a.out + i0 + t) : 0u;  // L2 hits
+    const int cpt0 = fuse ? (int)ld_h<true>(a.cpt + i0 + t) : 0;
 #elif RGBDSEG_FUSE_LOAD == 2
     const uint32_t out0 = r.out0;
     const int cpt0 = (int)(int8_t)r.cpt0;
@@ -545,6 +549,11 @@ __device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i0, unsig
 #if RGBDSEG_FUSE_LOAD == 2
     r.out0 = a.fuse ? ld_h<kElide>(a.out + i0 + t) : 0u;
     r.cpt0 = a.fuse ? (uint32_t)(uint8_t)ld_h<kElide>(a.cpt + i0 + t) : 0u;
+#elif RGBDSEG_FUSE_LOAD == 3
+    if (kLean || a.fuse) {  // fusion state into L2 now, read at List 1 from L2
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a.out + i0 + t));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a.cpt + i0 + t));
+    }
 #else
     if (kLean || a.fuse) {  // fusion state into L1 now (no registers held), read at List 1
         asm volatile("prefetch.global.L1 [%0];" ::"l"(a.out + i0 + t));
