@@ -10,6 +10,9 @@
 //   rgbdseg::FusionState, reset_state,   rgbdseg::b200::FusionState,     fusion.hpp:11-23
 //            fuse_step                            reset_state, fuse_step
 //   rgbdseg::SequenceProcessor           rgbdseg::b200::SequenceProcessor processor.hpp:60-80
+//   rgbdseg::init_mixture, match_        rgbdseg::b200::init_mixture,    mixture.hpp:43-60
+//            component, update_mixture,           match_component, ... (+ batched
+//            classify, step_pixel                 *_mixtures forms over spans)
 //
 // Same signatures, argument meaning, return types and exception types
 // (std::invalid_argument with the reference's messages), so a call site
@@ -28,7 +31,9 @@
 #include <memory>
 #include <optional>
 #include <stdexcept>
+#include <span>
 #include <string>
+#include <vector>
 
 #include "rgbdseg/processor.hpp"
 #include "rgbdseg_c.h"
@@ -292,6 +297,87 @@ inline MaskPlane fuse_step(FusionState& state, const MaskPlane& rgb_mask,
 // the reference (same results, test_segmenter.cpp:186-206) and, like it,
 // exposes no ModelBank (color_bank() / depth_bank() return nullptr) and
 // rejects the augmented method.
+// ---- per-pixel API (mixture.hpp:43-60) ----------------------------------
+// The reference's PixelMixture and the C-ABI record share one layout
+// (int, int, float[20], float[5], float[5]).  Every single-record call is a
+// GPU round trip, which only makes sense for parity checks; the batched
+// forms below run one kernel over all records.
+static_assert(sizeof(PixelMixture) == sizeof(rgbdseg_pixel_mixture), "record layout");
+inline rgbdseg_pixel_mixture* rec(PixelMixture* m) {
+    return reinterpret_cast<rgbdseg_pixel_mixture*>(m);
+}
+inline const rgbdseg_pixel_mixture* rec(const PixelMixture* m) {
+    return reinterpret_cast<const rgbdseg_pixel_mixture*>(m);
+}
+
+inline PixelMixture init_mixture(std::span<const float> first_value, const MixtureConfig& config,
+                                 int device = 0) {
+    const rgbdseg_mixture_cfg c = to_c(config);
+    PixelMixture m;
+    check(rgbdseg_init_mixtures(first_value.data(), (int)first_value.size(), 1, &c, rec(&m),
+                                device));
+    return m;
+}
+
+inline std::optional<int> match_component(const PixelMixture& mixture,
+                                          std::span<const float> value,
+                                          const MixtureConfig& config, int device = 0) {
+    const rgbdseg_mixture_cfg c = to_c(config);
+    int32_t k = -1;
+    check(rgbdseg_match_components(rec(&mixture), value.data(), (int)value.size(), 1, &c, &k,
+                                   device));
+    return k < 0 ? std::nullopt : std::optional<int>(k);
+}
+
+inline void update_mixture(PixelMixture& mixture, std::span<const float> value,
+                           std::optional<int> matched, const MixtureConfig& config,
+                           int device = 0) {
+    const rgbdseg_mixture_cfg c = to_c(config);
+    const int32_t k = matched ? *matched : -1;
+    check(rgbdseg_update_mixtures(rec(&mixture), value.data(), (int)value.size(), 1, &k, &c,
+                                  device));
+}
+
+inline PixelLabel classify(const PixelMixture& mixture, std::optional<int> matched,
+                           const MixtureConfig& config, int device = 0) {
+    const rgbdseg_mixture_cfg c = to_c(config);
+    const int32_t k = matched ? *matched : -1;
+    uint8_t lab = 1;
+    check(rgbdseg_classify_mixtures(rec(&mixture), &k, 1, &c, &lab, device));
+    return lab ? PixelLabel::Foreground : PixelLabel::Background;
+}
+
+inline PixelLabel step_pixel(PixelMixture& mixture, std::span<const float> value,
+                             const MixtureConfig& config, int device = 0) {
+    const rgbdseg_mixture_cfg c = to_c(config);
+    uint8_t lab = 1;
+    check(rgbdseg_step_mixtures(rec(&mixture), value.data(), (int)value.size(), 1, &c, &lab,
+                                device));
+    return lab ? PixelLabel::Foreground : PixelLabel::Background;
+}
+
+// Batched: record i observes values[i*C .. i*C+C).
+inline void step_mixtures(std::span<PixelMixture> mixtures, std::span<const float> values,
+                          int channels, const MixtureConfig& config, std::span<PixelLabel> labels,
+                          int device = 0) {
+    if (values.size() != mixtures.size() * (size_t)channels || labels.size() != mixtures.size())
+        throw std::invalid_argument("step_mixtures: size mismatch");
+    const rgbdseg_mixture_cfg c = to_c(config);
+    static_assert(sizeof(PixelLabel) == 1, "label layout");
+    check(rgbdseg_step_mixtures(rec(mixtures.data()), values.data(), channels, mixtures.size(), &c,
+                                reinterpret_cast<uint8_t*>(labels.data()), device));
+}
+
+inline std::vector<PixelMixture> init_mixtures(std::span<const float> values, int channels,
+                                               const MixtureConfig& config, int device = 0) {
+    if (channels <= 0 || values.size() % (size_t)channels)
+        throw std::invalid_argument("init_mixtures: size mismatch");
+    std::vector<PixelMixture> out(values.size() / channels);
+    const rgbdseg_mixture_cfg c = to_c(config);
+    check(rgbdseg_init_mixtures(values.data(), channels, out.size(), &c, rec(out.data()), device));
+    return out;
+}
+
 class SequenceProcessor {
 public:
     SequenceProcessor(int width, int height, const MethodSet& methods, const RunConfig& config,

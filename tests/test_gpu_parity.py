@@ -680,6 +680,24 @@ def test_cpp_dropin_is_source_compatible_with_run_scenario(cuda):
         assert "0 failure(s)" in r.stdout
 
 
+def test_cpp_dropin_per_pixel_api_matches_reference(cuda):
+    """integration/mixture_test: rgbdseg::b200::{init_mixture,
+    match_component, classify, update_mixture, step_pixel} and the batched
+    init_mixtures / step_mixtures against the reference's own functions
+    (mixture.cpp:58-154) on random sequences -> identical matches, labels and
+    records."""
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "integration", "_build", "mixture_test")
+    if not os.path.exists(exe):
+        pytest.skip("integration/_build/mixture_test not built (needs /root/reference)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "mismatches 0" in r.stdout
+
+
 # ------------------------------------------------------------ K2 registration
 
 def _rig_from_array(R, a):
