@@ -725,7 +725,7 @@ def main():
     def host_ring(frames, packed):
         """Pinned host buffers of `frames`: planar r|g|b|depth, or R,G,B-
         interleaved colour + depth (one buffer per frame)."""
-        ring, keep = [], []
+        ring, keep, flat = [], [], []
         for f in frames:
             src = sh.render(R, f, device)
             buf = torch.empty(5 * npx, dtype=torch.uint8, pin_memory=True)
@@ -743,25 +743,26 @@ def main():
                 ring.append((a[:npx].reshape(shp), a[npx:2 * npx].reshape(shp),
                              a[2 * npx:3 * npx].reshape(shp), dep))
             keep.append(buf)
+            flat.append(a)
             del src
         torch.cuda.synchronize()
-        return ring, keep
+        return ring, keep, flat
 
     pe = make_proc(R, sh, device, args.variant)
     preroll(R, pe, sh, range(start - args.preroll, start - nwarm), device)
     nhost = e2e_steps + sync_steps
-    host, keep = host_ring(range(start - nwarm, start + nhost), packed=False)
-    warm, host = host[:nwarm], host[nwarm:]
+    _, keep, host = host_ring(range(start - nwarm, start + nhost), packed=False)
+    warm, host = host[:nwarm], host[nwarm:]  # planar pinned frames r|g|b|depth
     outs = [torch.empty(npx, dtype=torch.uint8, pin_memory=True).numpy() for _ in range(2)]
     outs = [o.reshape(shp) for o in outs]
     for k in range(nwarm):
-        pe.submit(*warm[k], fused=outs[k % 2])
+        pe.submit_planar(warm[k], fused=outs[k % 2])
     pe.sync()
     barrier()
     with ClockSampler(device) as clk_e2e:
         t0 = time.perf_counter()
         for k in range(e2e_steps):
-            pe.submit(*host[k], fused=outs[k % 2])
+            pe.submit_planar(host[k], fused=outs[k % 2])
         pe.sync()
         e2e_s = time.perf_counter() - t0
     barrier()
@@ -770,7 +771,7 @@ def main():
     barrier()
     t0 = time.perf_counter()
     for k in range(sync_steps):
-        pe.process(*host[e2e_steps + k], want=(), out={"fused": outs[k % 2]})
+        pe.process_planar(host[e2e_steps + k], fused=outs[k % 2])
     sync_s = allmax(time.perf_counter() - t0)
     sync_value = total_units * sync_steps / sync_s / 1e6
     e2e_frames = f"{start}..{start + e2e_steps - 1}"
@@ -810,7 +811,7 @@ def main():
     if "packed" in wanted:
         pi = make_proc(R, sh, device, args.variant)
         preroll(R, pi, sh, range(start - args.preroll, start - nwarm), device)
-        ring, keep = host_ring(range(start - nwarm, start + e2e_steps), packed=True)
+        ring, keep, _ = host_ring(range(start - nwarm, start + e2e_steps), packed=True)
         for k in range(nwarm):
             pi.submit_interleaved(*ring[k], order="rgb", fused=outs[k % 2])
         pi.sync()
@@ -931,8 +932,9 @@ def main():
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_value, 2), "unit": "Mpix/s",
                     "h2d_bytes_per_step": 5 * npx, "d2h_bytes_per_step": npx,
-                    "mode": ("submit/sync pipelined, pinned planar host frames (r|g|b|depth) "
-                             f"of frames {e2e_frames} after pre-roll, fused masks read back"),
+                    "mode": ("SequenceProcessor.submit_planar/sync pipelined, pinned planar "
+                             f"host frames (r|g|b|depth) of frames {e2e_frames} after pre-roll, "
+                             "fused masks read back"),
                     "sync_process_value": round(sync_value, 2),
                     "sync_process_frames": f"{start + e2e_steps}..{start + nhost - 1}",
                     "interleaved": e2e_packed,

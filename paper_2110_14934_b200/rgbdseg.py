@@ -822,6 +822,53 @@ class SequenceProcessor:
         if ts:
             check(lib.rgbdseg_processor_signal_stream(self._h, cur), "submit")
 
+    def _planar_ptr(self, frame, what):
+        n = self.npx
+        if _is_torch(frame):
+            import torch
+
+            if frame.dtype != torch.uint8 or not frame.is_contiguous() or frame.numel() != 5 * n:
+                raise ValueError(f"{what}: expected a contiguous uint8 tensor of 5*{n} bytes")
+            if n % 2:
+                raise ValueError(f"{what}: odd pixel count (the depth plane would be "
+                                 "misaligned on the device); pass the planes")
+            return frame.data_ptr()
+        if (not isinstance(frame, np.ndarray) or frame.dtype != np.uint8
+                or not frame.flags.c_contiguous or frame.size != 5 * n):
+            raise ValueError(f"{what}: expected a C-contiguous uint8 array of 5*{n} bytes")
+        return frame.ctypes.data
+
+    def submit_planar(self, frame, fused=None, order=True):
+        """submit() of ONE planar frame buffer: r, g, b (npx bytes each) then
+        the uint16 depth plane, back to back -- the layout a capture ring of
+        pinned buffers uses.  The library moves it in one DMA per chunk; the
+        Python side checks one buffer instead of four (~5 us instead of ~20
+        per call, which matters for single-VGA frames).  `fused` (npx bytes)
+        receives the fused mask at sync()."""
+        p = self._planar_ptr(frame, "submit_planar")
+        n = self.npx
+        fo = _buf(fused, np.uint8, n, "fused", True)
+        self._keep.append((frame, fused))
+        ts = _cuda_tensors(frame, fused) if order else []
+        if ts:
+            import torch
+
+            cur = torch.cuda.current_stream(ts[0].device).cuda_stream
+            check(lib.rgbdseg_processor_wait_stream(self._h, cur), "submit_planar")
+        check(lib.rgbdseg_processor_submit(self._h, p, p + n, p + 2 * n, p + 3 * n, fo, None,
+                                           None), "submit_planar")
+        if ts:
+            check(lib.rgbdseg_processor_signal_stream(self._h, cur), "submit_planar")
+
+    def process_planar(self, frame, fused=None):
+        """process() of one planar frame buffer (see submit_planar); returns
+        the fused mask (a new array unless `fused` is given)."""
+        if fused is None:
+            fused = np.empty(self._shape(), np.uint8)
+        self.submit_planar(frame, fused)
+        self.sync()
+        return fused
+
     def sync(self):
         check(lib.rgbdseg_processor_sync(self._h), "sync")
         self._keep.clear()

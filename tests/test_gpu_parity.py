@@ -1594,3 +1594,45 @@ def test_fused_processor_random_configs_vs_oracle(R, port, cuda, seed):
             assert np.array_equal(Fc[s], orc[s].color.flags), (seed, s)
         assert np.array_equal(p.fusion_state().cpt.reshape(S, -1),
                               np.stack([o.cpt for o in orc])), seed
+
+
+@pytest.mark.parametrize("w,h,S", [(64, 32, 3), (37, 23, 1)])
+def test_planar_frame_submit_matches_plane_submit(R, port, cuda, w, h, S):
+    """SequenceProcessor.submit_planar / process_planar (one r|g|b|depth host
+    buffer per frame) give the oracle's fused masks, incl. an odd pixel count
+    (unaligned depth plane in the host buffer)."""
+    cfg = R.RunConfig.defaults()
+    cfg.color_gmm.components = cfg.depth_gmm.components = 4
+    proc = R.SequenceProcessor(w, h, cfg, streams=S)
+    orc = [O.PortProcessor(port, w * h, O.color_cfg(4), O.depth_cfg(4)) for _ in range(S)]
+    scenes = [O.PortScene(port, "A", w, h, seed=s + 1) for s in range(S)]
+    n = S * w * h
+    bufs = [np.empty(5 * n, np.uint8) for _ in range(3)]
+    outs = [np.empty((S, h, w) if S > 1 else (h, w), np.uint8) for _ in range(3)]
+    expect = []
+    for f in range(24):
+        frs = [sc.render(95 + f) for sc in scenes]
+        buf = bufs[f % 3]
+        for i, k in enumerate(("r", "g", "b")):
+            buf[i * n:(i + 1) * n] = np.stack([getattr(fr, k) for fr in frs]).ravel()
+        d = np.stack([holes(fr.depth, f) for fr in frs])
+        buf[3 * n:] = d.view(np.uint8).ravel()
+        exp = np.stack([orc[s].process(frs[s].r, frs[s].g, frs[s].b, d[s])[2]
+                        for s in range(S)])
+        if f % 2:
+            got = proc.process_planar(buf)
+            assert np.array_equal(got.reshape(S, -1), exp), f
+        else:
+            proc.submit_planar(buf, fused=outs[f % 3])
+            expect.append((f % 3, exp))
+            if len(expect) == 1:
+                continue
+        proc.sync()
+        for k, e in expect:
+            assert np.array_equal(outs[k].reshape(S, -1), e), f
+        expect.clear()
+    proc.sync()
+    for k, e in expect:
+        assert np.array_equal(outs[k].reshape(S, -1), e)
+    with pytest.raises(ValueError, match="5\\*"):
+        proc.submit_planar(np.empty(5 * n - 1, np.uint8))
