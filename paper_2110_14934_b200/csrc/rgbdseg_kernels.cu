@@ -351,6 +351,9 @@ __global__ void __launch_bounds__(kThreads)
 // Resident 128-thread blocks per SM: the dense variant is HBM-bound at 6
 // (72 regs, 24 warps/SM); the elided one is issue/latency-bound and gains
 // from 12 (40 regs, 48 warps/SM) despite spills (profiles/variants_r01.json).
+#ifndef RGBDSEG_CPRE_L1  // 1: colour components 0..kPre-1 via one L1 prefetch + L1 reads
+#define RGBDSEG_CPRE_L1 0
+#endif
 #ifndef RGBDSEG_PRE_COLOR  // colour components loaded with the flag words (2 or 3)
 #define RGBDSEG_PRE_COLOR 2
 #endif
@@ -478,7 +481,18 @@ __device__ __forceinline__ void fused_core(const FusedArgs& a, size_t i0, unsign
 #endif
     // ---- colour stream (segment_color) ----
     const float vc[3] = {r.vc[0], r.vc[1], r.vc[2]};
+#if RGBDSEG_CPRE_L1
+    Mixture<kPre, 3> cpre;  // L1 hits: the lines were prefetched in round one
+#pragma unroll
+    for (int i = 0; i < kPre; ++i) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) cpre.mu[i][c] = p.cs[(i * 3 + c) * kBlockPx];
+        cpre.var[i] = p.cs[(MC * 3 + i) * kBlockPx];
+        cpre.w[i] = p.cs[(MC * 3 + MC + i) * kBlockPx];
+    }
+#else
     const Mixture<kPre, 3>& cpre = r.cpre;
+#endif
     uint32_t cf1 = r.cf;
     bool replay = false;
     uint32_t lc =
@@ -560,7 +574,21 @@ __device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i0, unsig
         asm volatile("prefetch.global.L1 [%0];" ::"l"(a.cpt + i0 + t));
     }
 #endif
-#if RGBDSEG_R1_DEPTH_FIRST  // the depth step runs first: its words first
+#if RGBDSEG_CPRE_L1
+    {  // one warp instruction: lane k < 5*kPre prefetches line k of colour
+       // components 0..kPre-1 (means, then variances, then weights)
+        const unsigned lane = t % kBlockPx;
+        constexpr unsigned kL = 5 * kPre;
+        if (kElide && lane < kL) {
+            const unsigned pl = lane < 3 * kPre ? lane
+                                : (lane < 4 * kPre ? MC * 3 + (lane - 3 * kPre)
+                                                   : MC * 4 + (lane - 4 * kPre));
+            const char* line = reinterpret_cast<const char*>(p.cs - lane) + pl * 128;
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(line));
+        }
+    }
+    load_mix<MD, kElide>(p.ds, r.dpre);
+#elif RGBDSEG_R1_DEPTH_FIRST  // the depth step runs first: its words first
     load_mix<MD, kElide>(p.ds, r.dpre);
     load_mix<MC, kElide>(p.cs, r.cpre);
 #else
