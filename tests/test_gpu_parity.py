@@ -1636,3 +1636,74 @@ def test_planar_frame_submit_matches_plane_submit(R, port, cuda, w, h, S):
         assert np.array_equal(outs[k].reshape(S, -1), e)
     with pytest.raises(ValueError, match="5\\*"):
         proc.submit_planar(np.empty(5 * n - 1, np.uint8))
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_scenes_vs_compiled_reference(R, ref, cuda, seed, tmp_path):
+    """Soak: random ScenarioSpecs (1-4 moving objects, illumination steps,
+    shadows, flicker, sensor noise) rendered by the reference's own renderer,
+    240 frames with depth holes, random component counts -- the GPU
+    processor (host frames) against the reference's SequenceProcessor
+    compiled from its sources: fused masks every frame, final banks and flags
+    bit-identical."""
+    import ctypes as C
+    import json as _json
+
+    rng = np.random.default_rng(500 + seed)
+    w, h, F = 72, 54, 240
+
+    def region():
+        x, y = int(rng.integers(0, w - 8)), int(rng.integers(0, h - 8))
+        return {"x": x, "y": y, "w": int(rng.integers(6, w - x + 1)), "h": int(rng.integers(6, h - y + 1))}
+
+    def span():
+        a = int(rng.integers(0, F - 10))
+        return a, int(rng.integers(a + 3, min(F, a + 60)))
+
+    objs = []
+    for _ in range(int(rng.integers(1, 5))):
+        wp = sorted({int(v) for v in rng.integers(0, F, 3)} | {0, F - 1})
+        ow, oh = int(rng.integers(4, 20)), int(rng.integers(4, 16))
+        objs.append({"width": ow, "height": oh, "depth_offset_mm": int(rng.integers(100, 900)),
+                     "color": [int(v) for v in rng.integers(0, 256, 3)],
+                     "waypoints": [{"frame": f, "x": float(rng.uniform(0, w - ow - 1)),
+                                    "y": float(rng.uniform(0, h - oh - 1))} for f in wp]})
+    spec = {"name": f"soak{seed}", "width": w, "height": h, "frame_count": F, "seed": seed + 1,
+            "objects": objs,
+            "illumination": [dict(zip(("start", "end"), span()), gain=float(rng.uniform(0.5, 1.6)))
+                             for _ in range(int(rng.integers(0, 3)))],
+            "shadows": [dict(zip(("start", "end"), span()), region=region(),
+                             darken=float(rng.uniform(0.4, 0.9)))
+                        for _ in range(int(rng.integers(0, 3)))],
+            "flicker": [dict(zip(("start", "end"), span()), region=region(),
+                             color_sigma=float(rng.uniform(0, 6)),
+                             depth_sigma_mm=float(rng.uniform(0, 40)))
+                        for _ in range(int(rng.integers(0, 2)))],
+            "noise": {"color_sigma": float(rng.uniform(0, 3)), "depth_sigma_mm": float(rng.uniform(0, 5))}}
+    path = tmp_path / "spec.json"
+    path.write_text(_json.dumps(spec))
+    ref.lib.rref_scene_from_json.restype = C.c_void_p
+    ref.lib.rref_scene_from_json.argtypes = [C.c_char_p]
+    sh = ref.lib.rref_scene_from_json(str(path).encode())
+    assert sh, ref.lib.rref_last_error()
+    mc, md = int(rng.integers(3, 6)), int(rng.integers(3, 6))
+    cfg = R.RunConfig.defaults()
+    cfg.color_gmm.components, cfg.depth_gmm.components = mc, md
+    proc = R.SequenceProcessor(w, h, cfg)
+    rp = O.RefProcessor(ref, w, h, O.color_cfg(mc), O.depth_cfg(md))
+    try:
+        for f in range(F):
+            fr = {k: np.empty((h, w), np.uint16 if k == "depth" else np.uint8)
+                  for k in ("r", "g", "b", "depth", "gt")}
+            ref.check(ref.lib.rref_render(sh, f, fr["r"], fr["g"], fr["b"], fr["depth"],
+                                          fr["gt"].ctypes.data))
+            d = holes(fr["depth"], f)
+            fm = proc.process(fr["r"], fr["g"], fr["b"], d, want=("fused",))
+            _, _, fu = rp.process(fr["r"], fr["g"], fr["b"], d, want_masks=False)
+            assert np.array_equal(fm.fused.ravel(), fu), (seed, f)
+    finally:
+        ref.lib.rref_scene_destroy(sh)
+    assert proc.color_bank().planes().tobytes() == rp.bank_planes(0).tobytes()
+    assert proc.depth_bank().planes().tobytes() == rp.bank_planes(1).tobytes()
+    assert np.array_equal(proc.color_bank().initialized_plane().ravel(), rp.flags(0))
+    assert np.array_equal(proc.depth_bank().initialized_plane().ravel(), rp.flags(1))
