@@ -194,6 +194,28 @@ __device__ __forceinline__ void store_mix_elide(float* s, const Mixture<N, C>& m
             st_h<H>(s + (L * C + L + i) * kBlockPx, m.w[i]);
 }
 
+// store_mix_elide without the old weights: every real component's weight is
+// stored; the untouched last component (kVirt) only when it stops being +0.
+#ifndef RGBDSEG_WSTORE_ALL
+#define RGBDSEG_WSTORE_ALL 1  // +0.6% mid-sequence, +3% late (variants_r02.json)
+#endif
+template <int L, bool H, bool kVirt, int N, int C>
+__device__ __forceinline__ void store_mix_elide_wall(float* s, const Mixture<N, C>& m,
+                                                     int touched) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        if (touched == i) {
+#pragma unroll
+            for (int c = 0; c < C; ++c) st_h<H>(s + (i * C + c) * kBlockPx, m.mu[i][c]);
+            st_h<H>(s + (L * C + i) * kBlockPx, m.var[i]);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+        if (!(kVirt && i == N - 1) || __float_as_uint(m.w[i]) != 0u)
+            st_h<H>(s + (L * C + L + i) * kBlockPx, m.w[i]);
+}
+
 // Exact replay of a pixel the fast step refused: the whole mixture from
 // memory (nothing was stored) through the generic gmm_step.  K1 runs it once
 // per bank after both fast steps, so there is one inlined copy per bank
@@ -236,14 +258,21 @@ __device__ __forceinline__ uint32_t step_pixel_n(float* s, const Mixture<(P > 0 
         m.var[i] = pre.var[i];
         m.w[i] = pre.w[i];
     }
+    // RGBDSEG_WSTORE_ALL: with two or more real components the renormalised
+    // weights change on (almost) every step, so their old bits are not kept
+    // live to elide the store; the untouched last component still compares
+    // with its known +0.
+    constexpr bool kWAll = RGBDSEG_WSTORE_ALL && kElide && (kVirt ? N - 1 : N) >= 2;
     float w_old[N];
 #pragma unroll
-    for (int q = 0; q < N; ++q) w_old[q] = m.w[q];
+    for (int q = 0; q < N; ++q) w_old[q] = kWAll ? 0.0f : m.w[q];
     int t = 0;
     bool ok = k.fast != 0;
     const uint32_t label = gmm_step_fast<N, C, kVirt>(m, v, k, t, ok);
     if (ok) {
-        if (kElide)
+        if (kWAll) {
+            store_mix_elide_wall<M, kElide, kVirt>(s, m, t);
+        } else if (kElide)
             store_mix_elide<M, kElide>(s, m, t, w_old);
         else
             store_mix<M, kElide>(s, m);
