@@ -52,7 +52,8 @@ __device__ __forceinline__ void step2_n(float* s, const Mixture<(P > 0 ? P : 1),
         for (int i = 0; i < N; ++i) w_old[q][i] = m[q].w[i];
         t[q] = 0;
         ok[q] = k.fast != 0;
-        lab[q] = gmm_step_fast<N, C, kVirt>(m[q], v[q], k, t[q], ok[q]);
+        float mo[C], vo;
+        lab[q] = gmm_step_fast<N, C, kVirt>(m[q], v[q], k, t[q], ok[q], mo, vo);
     }
 #pragma unroll
     for (int q = 0; q < 2; ++q) {

@@ -196,6 +196,9 @@ __device__ __forceinline__ void store_mix_elide(float* s, const Mixture<N, C>& m
 
 // store_mix_elide without the old weights: every real component's weight is
 // stored; the untouched last component (kVirt) only when it stops being +0.
+#ifndef RGBDSEG_DIRECT_ST  // 1: touched mean/variance stored at a computed address
+#define RGBDSEG_DIRECT_ST 1  // spills 752 -> 332 B, VGA +8%, late +0.6% (variants_r02.json)
+#endif
 #ifndef RGBDSEG_WSTORE_ALL
 #define RGBDSEG_WSTORE_ALL 1  // +0.6% mid-sequence, +3% late (variants_r02.json)
 #endif
@@ -263,14 +266,29 @@ __device__ __forceinline__ uint32_t step_pixel_n(float* s, const Mixture<(P > 0 
     // live to elide the store; the untouched last component still compares
     // with its known +0.
     constexpr bool kWAll = RGBDSEG_WSTORE_ALL && kElide && (kVirt ? N - 1 : N) >= 2;
+    // RGBDSEG_DIRECT_ST: the touched component's new mean/variance are
+    // stored at its index (computed address) instead of written back into
+    // the mixture and stored by N predicated groups.
+    constexpr bool kDirect = RGBDSEG_DIRECT_ST && kElide;
     float w_old[N];
 #pragma unroll
     for (int q = 0; q < N; ++q) w_old[q] = kWAll ? 0.0f : m.w[q];
     int t = 0;
     bool ok = k.fast != 0;
-    const uint32_t label = gmm_step_fast<N, C, kVirt>(m, v, k, t, ok);
+    float mu_o[C], var_o;
+    const uint32_t label = gmm_step_fast<N, C, kVirt, kDirect>(m, v, k, t, ok, mu_o, var_o);
     if (ok) {
-        if (kWAll) {
+        if (kDirect) {
+            float* pm = s + t * (C * kBlockPx);
+#pragma unroll
+            for (int c = 0; c < C; ++c) st_h<kElide>(pm + c * kBlockPx, mu_o[c]);
+            st_h<kElide>(s + (M * C + t) * kBlockPx, var_o);
+#pragma unroll
+            for (int i = 0; i < N; ++i)
+                if (kWAll ? (!(kVirt && i == N - 1) || __float_as_uint(m.w[i]) != 0u)
+                          : __float_as_uint(m.w[i]) != __float_as_uint(w_old[i]))
+                    st_h<kElide>(s + (M * C + M + i) * kBlockPx, m.w[i]);
+        } else if (kWAll) {
             store_mix_elide_wall<M, kElide, kVirt>(s, m, t);
         } else if (kElide)
             store_mix_elide<M, kElide>(s, m, t, w_old);
