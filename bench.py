@@ -1,7 +1,7 @@
 """bench.py -- fused RGB-D GMM segmentation throughput on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload streams256|vga|hd1080|rows8k] [--variant auto|ldg|ldg_elide]
+                    [--workload streams256|vga|hd1080|rows8k] [--variant auto|ldg|ldg_elide|ldg_elide_l1]
 
 One step = one frame of every camera stream of the workload pushed through
 the hot path (colour GMM + depth GMM + List-1 fusion, processor.cpp:158-184).
@@ -524,7 +524,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="streams256", choices=sorted(WORKLOADS))
-    ap.add_argument("--variant", default="auto", choices=["auto", "ldg", "ldg_elide"])
+    ap.add_argument("--variant", default="auto", choices=["auto", "ldg", "ldg_elide", "ldg_elide_l1"])
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = auto (host ring <= 4 GB)")
     ap.add_argument("--start", type=int, default=START_FRAME,
                     help="first warm-up frame of scenario A (timed frames follow the warm-up)")

@@ -281,11 +281,14 @@ void* rgbdseg_processor_stream(rgbdseg_processor* p);
  * `stream` wait for everything the processor has queued so far. */
 int rgbdseg_processor_wait_stream(rgbdseg_processor* p, void* stream);
 int rgbdseg_processor_signal_stream(rgbdseg_processor* p, void* stream);
-/* Kernel variant: 0 = auto (= 2), 1 = dense: reads and writes back every
- * state word, 2 = elided: reads only the components the flag words mark as
- * touched, runs the step on the warp's touched prefix and rewrites only the
- * words whose bits changed.  Every variant produces the same bits; they
- * differ only in HBM traffic and instruction count. */
+/* Kernel variant: 0 = auto (2 for launches under 4 occupancy waves, else 3),
+ * 1 = dense: reads and writes back every state word, 2 = elided: reads only
+ * the components the flag words mark as touched, runs the step on the warp's
+ * touched prefix and rewrites only the words whose bits changed, 3 = elided
+ * with colour components 0..1 prefetched into L1 in the first load round and
+ * read at the colour step (fewer registers live through the depth step).
+ * Every variant produces the same bits; they differ only in HBM traffic,
+ * instruction count and register use. */
 int rgbdseg_processor_set_variant(rgbdseg_processor* p, int variant);
 /* Near-threshold report (north_star's parity accounting).  With rel > 0,
  * every later step first counts -- on the state before the step, in a

@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(HERE, "librgbdseg_b200.so")
 OK, EINVAL, ECUDA, ENOMEM, ERUNTIME = 0, 1, 2, 3, 4
 COLOR3, DEPTH1, AUGMENTED4 = 0, 1, 2
 FLAGS_PLANE = -1
-VARIANTS = {"auto": 0, "ldg": 1, "ldg_elide": 2}
+VARIANTS = {"auto": 0, "ldg": 1, "ldg_elide": 2, "ldg_elide_l1": 3}
 ORDER = {"rgb": 0, "bgr": 1}
 
 

@@ -1361,7 +1361,7 @@ int rgbdseg_processor_near_threshold_counts(rgbdseg_processor* p, uint64_t* colo
 
 int rgbdseg_processor_set_variant(rgbdseg_processor* p, int variant) {
     if (!p) return fail(RGBDSEG_EINVAL, "processor_set_variant: null handle");
-    if (variant < kAuto || variant > kLdgElide) return fail(RGBDSEG_EINVAL, "unknown kernel variant");
+    if (variant < kAuto || variant > kLdgElideL1) return fail(RGBDSEG_EINVAL, "unknown kernel variant");
     p->variant = variant;
     return RGBDSEG_OK;
 }

@@ -398,8 +398,16 @@ __global__ void __launch_bounds__(kThreads)
 // Resident 128-thread blocks per SM: the dense variant is HBM-bound at 6
 // (72 regs, 24 warps/SM); the elided one is issue/latency-bound and gains
 // from 12 (40 regs, 48 warps/SM) despite spills (profiles/variants_r01.json).
-#ifndef RGBDSEG_CPRE_L1  // 1: colour components 0..kPre-1 via one L1 prefetch + L1 reads
-#define RGBDSEG_CPRE_L1 0
+// Launches of at least this many occupancy waves run K1's kL1 form: colour
+// components 0..kPre-1 prefetched into L1 by one warp instruction in round
+// one and read at the colour step, instead of held in registers through the
+// depth step.  With fewer registers live, large launches gain (+5.6% on
+// 256 x VGA, +3.5% at 1080p, +1.2% late in a sequence); a launch of one or
+// two waves is a single latency chain per warp, where the extra L1 round
+// trip costs (-6% on one VGA frame) -- profiles/variants_r02.json.
+// 0 disables the kL1 form.
+#ifndef RGBDSEG_L1_MIN_WAVES
+#define RGBDSEG_L1_MIN_WAVES 4
 #endif
 #ifndef RGBDSEG_PRE_COLOR  // colour components loaded with the flag words (2 or 3)
 #define RGBDSEG_PRE_COLOR 2
@@ -477,7 +485,7 @@ struct PixAddr {
 #ifndef RGBDSEG_FUSE_SEL  // 1: List 1 as selects (fuse_pixel_sel) in K1 (measured 1-2% slower)
 #define RGBDSEG_FUSE_SEL 0
 #endif
-template <int MC, int MD, bool kElide, bool kLean = false>
+template <int MC, int MD, bool kElide, bool kLean = false, bool kL1 = false>
 __device__ __forceinline__ void fused_core(const FusedArgs& a, size_t i0, unsigned t,
                                            const PixAddr<MC, MD>& p, const Round1& r,
                                            uint32_t (&lab)[3]) {
@@ -528,18 +536,19 @@ __device__ __forceinline__ void fused_core(const FusedArgs& a, size_t i0, unsign
 #endif
     // ---- colour stream (segment_color) ----
     const float vc[3] = {r.vc[0], r.vc[1], r.vc[2]};
-#if RGBDSEG_CPRE_L1
-    Mixture<kPre, 3> cpre;  // L1 hits: the lines were prefetched in round one
+    // kL1: colour components 0..kPre-1 were prefetched into L1 in round one
+    // (not held in registers through the depth step); read them now.
+    Mixture<kPre, 3> cl1;
+    if constexpr (kL1) {
 #pragma unroll
-    for (int i = 0; i < kPre; ++i) {
+        for (int i = 0; i < kPre; ++i) {
 #pragma unroll
-        for (int c = 0; c < 3; ++c) cpre.mu[i][c] = p.cs[(i * 3 + c) * kBlockPx];
-        cpre.var[i] = p.cs[(MC * 3 + i) * kBlockPx];
-        cpre.w[i] = p.cs[(MC * 3 + MC + i) * kBlockPx];
+            for (int c = 0; c < 3; ++c) cl1.mu[i][c] = p.cs[(i * 3 + c) * kBlockPx];
+            cl1.var[i] = p.cs[(MC * 3 + i) * kBlockPx];
+            cl1.w[i] = p.cs[(MC * 3 + MC + i) * kBlockPx];
+        }
     }
-#else
-    const Mixture<kPre, 3>& cpre = r.cpre;
-#endif
+    const Mixture<kPre, 3>& cpre = kL1 ? cl1 : r.cpre;
     uint32_t cf1 = r.cf;
     bool replay = false;
     uint32_t lc =
@@ -588,7 +597,8 @@ __device__ __forceinline__ void fused_core(const FusedArgs& a, size_t i0, unsign
 #ifndef RGBDSEG_R1_DEPTH_FIRST  // 1: issue the depth component before the colour ones
 #define RGBDSEG_R1_DEPTH_FIRST 0
 #endif
-template <int MC, int MD, bool kElide, bool kPacked = false, bool kLean = false>
+template <int MC, int MD, bool kElide, bool kPacked = false, bool kLean = false,
+          bool kL1 = false>
 __device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i0, unsigned t,
                                             uint32_t (&lab)[3]) {
     const PixAddr<MC, MD> p(a, i0, t);
@@ -621,33 +631,35 @@ __device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i0, unsig
         asm volatile("prefetch.global.L1 [%0];" ::"l"(a.cpt + i0 + t));
     }
 #endif
-#if RGBDSEG_CPRE_L1
-    {  // one warp instruction: lane k < 5*kPre prefetches line k of colour
-       // components 0..kPre-1 (means, then variances, then weights)
+    if constexpr (kL1) {
+        // one warp instruction: lane k < 5*kPre prefetches line k of colour
+        // components 0..kPre-1 (means, then variances, then weights)
         const unsigned lane = t % kBlockPx;
         constexpr unsigned kL = 5 * kPre;
-        if (kElide && lane < kL) {
+        if (lane < kL) {
             const unsigned pl = lane < 3 * kPre ? lane
                                 : (lane < 4 * kPre ? MC * 3 + (lane - 3 * kPre)
                                                    : MC * 4 + (lane - 4 * kPre));
             const char* line = reinterpret_cast<const char*>(p.cs - lane) + pl * 128;
             asm volatile("prefetch.global.L1 [%0];" ::"l"(line));
         }
-    }
-    load_mix<MD, kElide>(p.ds, r.dpre);
-#elif RGBDSEG_R1_DEPTH_FIRST  // the depth step runs first: its words first
-    load_mix<MD, kElide>(p.ds, r.dpre);
-    load_mix<MC, kElide>(p.cs, r.cpre);
+        load_mix<MD, kElide>(p.ds, r.dpre);
+    } else {
+#if RGBDSEG_R1_DEPTH_FIRST  // the depth step runs first: its words first
+        load_mix<MD, kElide>(p.ds, r.dpre);
+        load_mix<MC, kElide>(p.cs, r.cpre);
 #else
-    load_mix<MC, kElide>(p.cs, r.cpre);
-    load_mix<MD, kElide>(p.ds, r.dpre);
+        load_mix<MC, kElide>(p.cs, r.cpre);
+        load_mix<MD, kElide>(p.ds, r.dpre);
 #endif
-    fused_core<MC, MD, kElide, kLean>(a, i0, t, p, r, lab);
+    }
+    fused_core<MC, MD, kElide, kLean, kL1>(a, i0, t, p, r, lab);
 }
 
 // kEval: with the evaluation epilogue (a.gt set).  A separate instantiation,
 // so the plain kernel's register allocation carries none of it (measured 6%).
-template <int MC, int MD, bool kElide, bool kEval, bool kPacked = false, bool kLean = false>
+template <int MC, int MD, bool kElide, bool kEval, bool kPacked = false, bool kLean = false,
+          bool kL1 = false>
 __global__ void __launch_bounds__(kThreads, RGBDSEG_FUSED_MIN_BLOCKS(kElide))
     k_fused_ldg(const __grid_constant__ FusedArgs a) {
     const size_t i0 = (size_t)blockIdx.x * kThreads;
@@ -671,7 +683,7 @@ __global__ void __launch_bounds__(kThreads, RGBDSEG_FUSED_MIN_BLOCKS(kElide))
         }
     }
     uint32_t lab[3] = {0u, 0u, 0u};
-    if (active) fused_pixel<MC, MD, kElide, kPacked, kLean>(a, i0, threadIdx.x, lab);
+    if (active) fused_pixel<MC, MD, kElide, kPacked, kLean, kL1>(a, i0, threadIdx.x, lab);
     if constexpr (kEval) {  // evaluation epilogue: the masks never leave registers
         const uint32_t g = active ? (uint32_t)a.gt[i] : 0u;
         eval_accumulate<3>(active, a.base + i, a.stream_px, lab, g, a.counts);
@@ -1277,8 +1289,26 @@ cudaError_t go(K kernel, size_t n, cudaStream_t s, Args... args) {
     return cudaGetLastError();
 }
 
+// Whether a K1 launch over n pixels is large enough for the kL1 form: n at
+// least RGBDSEG_L1_MIN_WAVES occupancy waves of the elided kernel (12
+// resident 128-pixel blocks per SM) on the launching device.
+bool l1_form(size_t n) {
+    if (RGBDSEG_L1_MIN_WAVES <= 0) return false;
+    constexpr int kMaxDev = 64;
+    static std::atomic<int> sms_cache[kMaxDev];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int sms = dev < kMaxDev ? sms_cache[dev].load(std::memory_order_relaxed) : 0;
+    if (sms <= 0) {
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (dev < kMaxDev) sms_cache[dev].store(sms, std::memory_order_relaxed);
+    }
+    const size_t wave = (size_t)sms * RGBDSEG_ELIDE_MINB * kThreads;
+    return n >= (size_t)RGBDSEG_L1_MIN_WAVES * wave;
+}
+
 template <int MC, int MD>
-cudaError_t fused_ldg_md(const FusedArgs& a, bool elide, cudaStream_t s) {
+cudaError_t fused_ldg_md(const FusedArgs& a, bool elide, int variant, cudaStream_t s) {
     if (a.n == 0) return cudaSuccess;
     const unsigned nb = blocks_for(a.n);
     if (a.packed) {  // interleaved colour input (no evaluation epilogue)
@@ -1294,10 +1324,15 @@ cudaError_t fused_ldg_md(const FusedArgs& a, bool elide, cudaStream_t s) {
 #elif RGBDSEG_PIPE
             k_fused_pipe<MC, MD><<<pipe_blocks<MC, MD>(a.n), kThreads, 0, s>>>(a);
 #else
-            if (RGBDSEG_LEAN && a.fuse && !a.rgb_mask && !a.depth_mask && !a.fused_copy)
-                k_fused_ldg<MC, MD, true, false, false, true><<<nb, kThreads, 0, s>>>(a);
-            else
-                k_fused_ldg<MC, MD, true, false><<<nb, kThreads, 0, s>>>(a);
+            const bool lean = RGBDSEG_LEAN && a.fuse && !a.rgb_mask && !a.depth_mask &&
+                              !a.fused_copy;
+            if (variant == kLdgElideL1 || (variant == kAuto && l1_form(a.n))) {
+                lean ? k_fused_ldg<MC, MD, true, false, false, true, true><<<nb, kThreads, 0, s>>>(a)
+                     : k_fused_ldg<MC, MD, true, false, false, false, true><<<nb, kThreads, 0, s>>>(a);
+            } else {
+                lean ? k_fused_ldg<MC, MD, true, false, false, true><<<nb, kThreads, 0, s>>>(a)
+                     : k_fused_ldg<MC, MD, true, false><<<nb, kThreads, 0, s>>>(a);
+            }
 #endif
         }
     } else {
@@ -1339,7 +1374,7 @@ cudaError_t fused_md(const FusedArgs& a0, int variant, cudaStream_t s) {
     }
     FusedArgs a = a0;
     a.ahead = (unsigned)wv;
-    return fused_ldg_md<MC, MD>(a, elide, s);
+    return fused_ldg_md<MC, MD>(a, elide, variant, s);
 }
 
 template <int MC>

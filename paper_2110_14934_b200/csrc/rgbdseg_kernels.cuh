@@ -86,10 +86,13 @@ struct FusedArgs {
     int bgr;
 };
 
-// Kernel variants of K1 (identical results; they differ in HBM writes).
-// Auto = LDG with write elision.  A TMA cp.async.bulk staging variant was
+// Kernel variants of K1 (identical results; they differ in HBM traffic and
+// register use).  A TMA cp.async.bulk staging variant was
 // measured and dropped (profiles/variants_r01.json).
-enum Variant { kAuto = 0, kLdgDense = 1, kLdgElide = 2 };
+// Auto = elided, in its L1 form (colour components 0..1 through L1, not held
+// in registers) for launches of at least RGBDSEG_L1_MIN_WAVES occupancy
+// waves; kLdgElide / kLdgElideL1 force one form (tests, A/B).
+enum Variant { kAuto = 0, kLdgDense = 1, kLdgElide = 2, kLdgElideL1 = 3 };
 
 // All launchers return cudaGetLastError() after the launch.
 cudaError_t launch_fused(const FusedArgs& a, int variant, cudaStream_t s);

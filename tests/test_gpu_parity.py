@@ -295,7 +295,7 @@ def test_fusion_truth_table(R):
 
 # ------------------------------------------------------------ fused processor (K1)
 
-@pytest.mark.parametrize("variant", ["ldg", "ldg_elide"])
+@pytest.mark.parametrize("variant", ["ldg", "ldg_elide", "ldg_elide_l1"])
 @pytest.mark.parametrize("name", [s[0] for s in SCENARIOS])
 def test_processor_scenarios_match_reference_golden(R, port, name, variant):
     """The fused kernel over whole golden sequences: every per-frame rgb /
@@ -319,7 +319,7 @@ def test_processor_scenarios_match_reference_golden(R, port, name, variant):
     assert sha256(db.planes(), db.initialized_plane()) == gold["depth_bank"]
 
 
-@pytest.mark.parametrize("variant", ["ldg", "ldg_elide"])
+@pytest.mark.parametrize("variant", ["ldg", "ldg_elide", "ldg_elide_l1"])
 def test_processor_multistream_device_vs_oracle(R, port, cuda, variant):
     """Config-4 shape in miniature: S streams (seeds 1..S) batched in one
     kernel over device-resident frames rendered by the GPU scene generator,
@@ -541,7 +541,7 @@ def test_8k_frame_sampled_exact_and_chunk_invariant(R, port, cuda):
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("variant", ["auto", "ldg"])
+@pytest.mark.parametrize("variant", ["auto", "ldg", "ldg_elide_l1"])
 def test_processor_tail_and_misaligned_inputs(R, port, cuda, variant):
     """Odd frame sizes (partial last block) and device planes at odd byte
     offsets give the oracle's bits."""
@@ -834,7 +834,7 @@ def test_confusion_counts_kernel(R):
 
 
 @pytest.mark.parametrize("registered", [True, False])
-@pytest.mark.parametrize("variant", ["auto", "ldg"])
+@pytest.mark.parametrize("variant", ["auto", "ldg", "ldg_elide_l1"])
 def test_processor_eval_epilogue_counts(R, cuda, registered, variant):
     """The fused epilogue's per-stream counts equal counts of the returned
     masks (device frames, odd stream size, host gt on odd frames)."""
@@ -884,7 +884,7 @@ def test_acceptance_quality_criteria_on_gpu(R, cuda, scenario):
 
 
 @pytest.mark.parametrize("mc,md", [(3, 5), (5, 3), (4, 4), (3, 3), (5, 4)])
-@pytest.mark.parametrize("variant", ["ldg", "auto"])
+@pytest.mark.parametrize("variant", ["ldg", "auto", "ldg_elide_l1"])
 def test_processor_mixed_component_counts(R, port, mc, md, variant):
     """Every (colour M, depth M) instantiation of K1 against the oracle,
     with non-default rates and a counter limit of 2."""
@@ -1070,7 +1070,7 @@ def check_untouched_invariant(bank, words, sigma0):
     assert not (words >> (8 + M)).any() and not ((words >> 8) & 1).any()
 
 
-@pytest.mark.parametrize("variant", ["auto", "ldg"])
+@pytest.mark.parametrize("variant", ["auto", "ldg", "ldg_elide_l1"])
 def test_untouched_mask_set_at_init_and_only_shrinks(R, port, variant):
     """K1 marks components 1..M-1 untouched when it initialises a pixel
     (depth: only where a return arrived), clears a component's bit when a
@@ -1117,7 +1117,7 @@ def test_untouched_mask_set_at_init_and_only_shrinks(R, port, variant):
         assert got.tobytes() == ops[s].depth.planes().tobytes()
 
 
-@pytest.mark.parametrize("variant", ["auto", "ldg"])
+@pytest.mark.parametrize("variant", ["auto", "ldg", "ldg_elide_l1"])
 def test_upload_and_bank_api_keep_the_mask_exact(R, port, variant):
     """An uploaded plane (a component written behind K1's back) clears the
     mask, so the next fused frames read the uploaded words; segment_color on
@@ -1213,7 +1213,7 @@ def set_flag_words(R, bank, words):
     torch.cuda.synchronize()
 
 
-@pytest.mark.parametrize("variant", ["auto", "ldg"])
+@pytest.mark.parametrize("variant", ["auto", "ldg", "ldg_elide_l1"])
 def test_fused_random_untouched_masks_vs_oracle(R, port, variant):
     """Arbitrary untouched masks -- suffixes of every length, non-suffix
     sets (the full-width path), touched components with weight +0 (fitness
@@ -1489,7 +1489,7 @@ def test_config5_8k_full_frames_row_tiles_vs_reference(R, cuda):
     _check_banks_vs_ref(ref, rp, [(p.color_bank(), p.depth_bank()) for p in procs], w * h, M)
 
 
-@pytest.mark.parametrize("variant", ["auto", "ldg"])
+@pytest.mark.parametrize("variant", ["auto", "ldg", "ldg_elide_l1"])
 def test_device_frames_without_outputs_lean_path(R, port, cuda, variant):
     """Device-resident frames processed with NO mask outputs launch K1's
     fused-mask-only instantiation (kLean; the bench's `value` path).  Across
@@ -1564,7 +1564,8 @@ def test_fused_processor_random_configs_vs_oracle(R, port, cuda, seed):
         setattr(cfg.depth_gmm, k, v)
     cfg.fusion_counter_limit = limit
     host = R.SequenceProcessor(w, h, cfg, streams=S)
-    dev = R.SequenceProcessor(w, h, cfg, streams=S)
+    # the device processor forces K1's L1 form (auto picks it only for large launches)
+    dev = R.SequenceProcessor(w, h, cfg, streams=S, variant="ldg_elide_l1")
     oc = O.color_cfg(kc.pop("components"), **kc)
     od = O.depth_cfg(kd.pop("components"), **kd)
     orc = [O.PortProcessor(port, w * h, oc, od, limit=limit) for _ in range(S)]
@@ -1689,7 +1690,7 @@ def test_random_scenes_vs_compiled_reference(R, ref, cuda, seed, tmp_path):
     mc, md = int(rng.integers(3, 6)), int(rng.integers(3, 6))
     cfg = R.RunConfig.defaults()
     cfg.color_gmm.components, cfg.depth_gmm.components = mc, md
-    proc = R.SequenceProcessor(w, h, cfg)
+    proc = R.SequenceProcessor(w, h, cfg, variant=("auto", "ldg_elide_l1")[seed % 2])
     rp = O.RefProcessor(ref, w, h, O.color_cfg(mc), O.depth_cfg(md))
     try:
         for f in range(F):
