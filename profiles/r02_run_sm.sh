@@ -1,0 +1,12 @@
+#!/bin/bash
+# Round 2: kL1 form with colour components 0..1 staged thread-privately in
+# shared memory by cp.async (RGBDSEG_L1_SMEM) instead of an L1 prefetch.
+O=gpurun_out/r2sm; mkdir -p $O
+L=paper_2110_14934_b200/librgbdseg_b200.so
+cp $L $O/orig.so
+cp build/sm.so $L
+timeout 1500 python -m pytest tests/test_gpu_parity.py -q -x -k "ldg_elide_l1 or random_configs or random_scenes or config3 or config4 or config5" > $O/pytest_sm.log 2>&1; echo "rc=$?" >> $O/pytest_sm.log
+cp $O/orig.so $L
+for W in streams256 hd1080; do
+  timeout 1500 bash profiles/ab.sh $O/ab_$W $W def11 sm > $O/ab_$W.txt 2>&1
+done
