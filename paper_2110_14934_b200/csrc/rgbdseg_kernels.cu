@@ -1311,12 +1311,17 @@ template <int MC, int MD>
 cudaError_t fused_ldg_md(const FusedArgs& a, bool elide, int variant, cudaStream_t s) {
     if (a.n == 0) return cudaSuccess;
     const unsigned nb = blocks_for(a.n);
+    const bool l1 = elide && (variant == kLdgElideL1 || (variant == kAuto && l1_form(a.n)));
     if (a.packed) {  // interleaved colour input (no evaluation epilogue)
         if (a.gt) return cudaErrorInvalidValue;
-        elide ? k_fused_ldg<MC, MD, true, false, true><<<nb, kThreads, 0, s>>>(a)
-              : k_fused_ldg<MC, MD, false, false, true><<<nb, kThreads, 0, s>>>(a);
+        if (!elide)
+            k_fused_ldg<MC, MD, false, false, true><<<nb, kThreads, 0, s>>>(a);
+        else if (l1)
+            k_fused_ldg<MC, MD, true, false, true, false, true><<<nb, kThreads, 0, s>>>(a);
+        else
+            k_fused_ldg<MC, MD, true, false, true><<<nb, kThreads, 0, s>>>(a);
     } else if (elide) {
-        if (a.gt) {
+        if (a.gt) {  // the evaluation instantiation keeps the register form (L1: -2.3%)
             k_fused_ldg<MC, MD, true, true><<<nb, kThreads, 0, s>>>(a);
         } else {
 #if RGBDSEG_PX == 2
@@ -1326,7 +1331,7 @@ cudaError_t fused_ldg_md(const FusedArgs& a, bool elide, int variant, cudaStream
 #else
             const bool lean = RGBDSEG_LEAN && a.fuse && !a.rgb_mask && !a.depth_mask &&
                               !a.fused_copy;
-            if (variant == kLdgElideL1 || (variant == kAuto && l1_form(a.n))) {
+            if (l1) {
                 lean ? k_fused_ldg<MC, MD, true, false, false, true, true><<<nb, kThreads, 0, s>>>(a)
                      : k_fused_ldg<MC, MD, true, false, false, false, true><<<nb, kThreads, 0, s>>>(a);
             } else {

@@ -413,7 +413,9 @@ def test_interleaved_ingest_matches_planar(R, port, cuda, w, h, S, chunks):
     M = 5
     cfg = R.RunConfig.defaults()
     cfg.color_gmm.components = cfg.depth_gmm.components = M
-    procs = {k: R.SequenceProcessor(w, h, cfg, streams=S, host_chunks=chunks)
+    # "bgr" and "dev" force K1's L1 form (auto picks it for large launches only)
+    procs = {k: R.SequenceProcessor(w, h, cfg, streams=S, host_chunks=chunks,
+                                    variant="ldg_elide_l1" if k in ("bgr", "dev") else "auto")
              for k in ("planar", "rgb", "bgr", "dev")}
     orc = O.PortProcessor(port, S * w * h, O.color_cfg(M), O.depth_cfg(M))
     scenes = [O.PortScene(port, "A", w, h, seed=s + 1) for s in range(S)]
