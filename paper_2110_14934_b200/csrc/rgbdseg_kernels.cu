@@ -396,12 +396,13 @@ __global__ void __launch_bounds__(kThreads)
 
 // ---------------------------------------------------------------- K1 fused
 // Resident 128-thread blocks per SM: the dense variant is HBM-bound at 6
-// (72 regs, 24 warps/SM); the elided one is issue/latency-bound and gains
-// from 12 (40 regs, 48 warps/SM) despite spills (profiles/variants_r01.json).
+// (72 regs, 24 warps/SM); the elided one is latency-bound and gains from 12
+// (40 regs, 48 warps/SM) despite spills (profiles/variants_r0{1,2}.json).
 // Launches of at least this many occupancy waves run K1's kL1 form: colour
-// components 0..kPre-1 prefetched into L1 by one warp instruction in round
-// one and read at the colour step, instead of held in registers through the
-// depth step.  With fewer registers live, large launches gain (+5.6% on
+// components 0..kPre-1 prefetched by one warp instruction in round one
+// (prefetch.global.L1; ncu shows the lines are served from L2 by the time
+// they are read) and read at the colour step, instead of held in registers
+// through the depth step.  With fewer registers live, large launches gain (+5.6% on
 // 256 x VGA, +3.5% at 1080p, +1.2% late in a sequence); a launch of one or
 // two waves is a single latency chain per warp, where the extra L1 round
 // trip costs (-6% on one VGA frame) -- profiles/variants_r02.json.
@@ -517,7 +518,7 @@ __device__ __forceinline__ void fused_core(const FusedArgs& a, size_t i0, unsign
 #endif
     // The two banks are independent (only List 1 needs both labels): the
     // small depth step runs first, while the colour components wait in
-    // registers.
+    // registers (or, in the kL1 form, in the memory system).
     // ---- depth stream (segment_depth): raw 0 = no return ----
     uint32_t ld = 0;
     if (r.raw != 0) {
