@@ -660,8 +660,8 @@ __device__ __forceinline__ void fused_pixel(const FusedArgs& a, size_t i0, unsig
 // kEval: with the evaluation epilogue (a.gt set).  A separate instantiation,
 // so the plain kernel's register allocation carries none of it (measured 6%).
 template <int MC, int MD, bool kElide, bool kEval, bool kPacked = false, bool kLean = false,
-          bool kL1 = false>
-__global__ void __launch_bounds__(kThreads, RGBDSEG_FUSED_MIN_BLOCKS(kElide))
+          bool kL1 = false, int kMinB = 0>
+__global__ void __launch_bounds__(kThreads, kMinB ? kMinB : RGBDSEG_FUSED_MIN_BLOCKS(kElide))
     k_fused_ldg(const __grid_constant__ FusedArgs a) {
     const size_t i0 = (size_t)blockIdx.x * kThreads;
     const size_t i = i0 + threadIdx.x;
@@ -1308,6 +1308,30 @@ bool l1_form(size_t n) {
     return n >= (size_t)RGBDSEG_L1_MIN_WAVES * wave;
 }
 
+// Launches of at least RGBDSEG_HUGE_WAVES occupancy waves (256 x VGA,
+// 8192^2) run the kL1 form at RGBDSEG_HUGE_MINB resident blocks: +0.5% on the
+// default window and +1.4% / +2.8% late on 256 x VGA / 8192^2, where 1080p
+// (9 waves) prefers 12 (profiles/variants_r02.json).
+#ifndef RGBDSEG_HUGE_WAVES
+#define RGBDSEG_HUGE_WAVES 40
+#endif
+#ifndef RGBDSEG_HUGE_MINB
+#define RGBDSEG_HUGE_MINB 16
+#endif
+bool huge_launch(size_t n) {
+    if (RGBDSEG_HUGE_WAVES <= 0) return false;
+    constexpr int kMaxDev = 64;
+    static std::atomic<int> sms_cache[kMaxDev];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int sms = dev < kMaxDev ? sms_cache[dev].load(std::memory_order_relaxed) : 0;
+    if (sms <= 0) {
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (dev < kMaxDev) sms_cache[dev].store(sms, std::memory_order_relaxed);
+    }
+    return n >= (size_t)RGBDSEG_HUGE_WAVES * sms * RGBDSEG_ELIDE_MINB * kThreads;
+}
+
 template <int MC, int MD>
 cudaError_t fused_ldg_md(const FusedArgs& a, bool elide, int variant, cudaStream_t s) {
     if (a.n == 0) return cudaSuccess;
@@ -1332,7 +1356,12 @@ cudaError_t fused_ldg_md(const FusedArgs& a, bool elide, int variant, cudaStream
 #else
             const bool lean = RGBDSEG_LEAN && a.fuse && !a.rgb_mask && !a.depth_mask &&
                               !a.fused_copy;
-            if (l1) {
+            if (l1 && huge_launch(a.n)) {  // 32 registers, 64 warps/SM
+                lean ? k_fused_ldg<MC, MD, true, false, false, true, true, RGBDSEG_HUGE_MINB>
+                           <<<nb, kThreads, 0, s>>>(a)
+                     : k_fused_ldg<MC, MD, true, false, false, false, true, RGBDSEG_HUGE_MINB>
+                           <<<nb, kThreads, 0, s>>>(a);
+            } else if (l1) {
                 lean ? k_fused_ldg<MC, MD, true, false, false, true, true><<<nb, kThreads, 0, s>>>(a)
                      : k_fused_ldg<MC, MD, true, false, false, false, true><<<nb, kThreads, 0, s>>>(a);
             } else {
